@@ -1,0 +1,179 @@
+/* sbpcg.h — C ABI of libsbpcg: circulant-preconditioned CG inside Split Bregman for
+ * parallel-imaging + compressed-sensing MRI, B200 (sm_100a) native.
+ *
+ * Method: Koolstra, van Gemert, Boernert, Webb, Remis, "Accelerating CS in Parallel
+ * Imaging Reconstructions Using an Efficient and Effective Circulant Preconditioner"
+ * (arXiv 1710.01758).  "PAPER.md:n" below cites line n of that paper's LaTeX source.
+ *
+ * ------------------------------------------------------------------------------------
+ * Data conventions (all entry points)
+ *   * complex = interleaved (re, im) float32 pairs (sb_c64), i.e. torch.complex64;
+ *   * images are row-major [B][d0][d1]; d0 is the phase-encode axis of line masks
+ *     (a line mask samples whole rows: "random line pattern ... in the
+ *     foot-head direction"), d1 is the readout;
+ *   * coil stacks are [B][C][d0][d1]; k-space is unshifted (DC at index 0) and
+ *     unitary-scaled: (F x)(nu) = N^{-1/2} sum_n x(n) exp(-2 pi i nu.n/n)  (reading A1);
+ *   * mask is uint8 0/1 over the k-space grid, one per problem ([B][d0][d1]) or shared
+ *     ([d0][d1], dims.mask_shared = 1);
+ *   * every array pointer may be HOST or DEVICE memory (detected with
+ *     cudaPointerGetAttributes).  Host arrays are staged through the context's device
+ *     buffers inside the call; device arrays must live on the context's device, be
+ *     16-byte aligned and C-contiguous.  Outputs must not alias inputs (SB_E_ARG).
+ *   * B independent problems are solved together, each with its own PCG scalars and
+ *     its own convergence (a converged problem is frozen; reading A26).
+ * Ownership: the context copies sens and mask at create (the caller may free them
+ * afterwards) and owns Lambda^{-1}, the workspace and the SB state; the caller owns
+ * every I/O buffer.  One context must not be used by two host threads at once.
+ * Streams: all work is enqueued on the CUDA stream given at create (NULL = legacy
+ * default stream).  sb_pcg_apply_A / sb_pcg_apply_Pinv / sb_encode with device
+ * pointers are asynchronous; every other call returns after the stream completed.
+ * Errors: every call returns an sb_status and never throws across the ABI.  CUDA errors
+ * are sticky (SB_E_CUDA): the context is then unusable; sb_last_error() explains.
+ * ------------------------------------------------------------------------------------
+ */
+#ifndef SBPCG_H
+#define SBPCG_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SBPCG_ABI_VERSION 1
+
+typedef struct sb_ctx sb_ctx;
+typedef struct { float re, im; } sb_c64;
+
+typedef enum {
+  SB_OK = 0,
+  SB_E_ARG = 1,              /* NULL/aliased/misaligned pointer, bad option value      */
+  SB_E_DIM = 2,              /* shape/batch/coils/levels inconsistent (levels must     */
+                             /* divide the shape, PAPER.md:117 W unitary on the grid) */
+  SB_E_UNSUPPORTED_SIZE = 3, /* an image axis is not in the FFT size set               */
+  SB_E_PARAM = 4,            /* gamma <= 0, mu < 0 or lambda < 0 (k >= gamma > 0)      */
+  SB_E_SINGULAR_K = 5,       /* min |k| <= 1e-14 or non-finite           */
+  SB_E_NONFINITE = 6,        /* NaN/Inf in a PCG recurrence scalar                     */
+  SB_E_INDEFINITE = 7,       /* <p, A p> <= 0 (A must be HPD)            */
+  SB_E_CUDA = 8,             /* CUDA runtime error (sticky)                            */
+  SB_E_NOMEM = 9,            /* device allocation failed                               */
+  SB_E_COMM = 10             /* reserved: coil-sharded communicator errors             */
+} sb_status;
+
+/* Problem geometry.  ndim = 2 (3 reserved).  shape = {d0, d1, 0}.  Supported axis
+ * lengths: 4, 8, 16, 32, 48, 64, 96, 128, 192, 256 (radix-2/3, reading A23). */
+typedef struct {
+  int32_t ndim;
+  int64_t shape[3];
+  int32_t batch;           /* B >= 1 independent problems                              */
+  int32_t wavelet_levels;  /* L-level orthonormal Haar W (reading A6), 2^L | d0, d1    */
+  int32_t mask_shared;     /* 1: one mask for all problems                             */
+} sb_dims;
+
+/* Create a context for  A = mu sum_c (R F S_c)^H R F S_c + lambda sum_d D_d^H D_d
+ * + gamma W^H W  (W^H W = I) and build the circulant
+ * preconditioner  M^{-1} = F^H diag{k}^{-1} F,  k = mu k_c + lambda k_d + gamma
+ * (PAPER.md:189-197), k_c by the circular-correlation form of PAPER.md:199-229 (reading
+ * A2), k_d = sum_d 4 sin^2(pi nu_d/n_d), built once in fp64 on the
+ * device ("constructed beforehand").
+ *   out     receives the context (NULL on failure)
+ *   dims    geometry, see sb_dims
+ *   coils   C >= 1
+ *   mask    uint8 [B or 1][d0][d1], values 0/1
+ *   sens    complex [B][C][d0][d1] coil sensitivities S_c
+ *   mu, lambda, gamma  weights of Eq. original; gamma > 0 required
+ *   cuda_stream  cudaStream_t to enqueue on (NULL = default stream)
+ * Errors: SB_E_ARG, SB_E_DIM, SB_E_UNSUPPORTED_SIZE, SB_E_PARAM, SB_E_SINGULAR_K,
+ *         SB_E_NOMEM, SB_E_CUDA.  Synchronises the stream before returning. */
+sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const uint8_t* mask,
+                        const sb_c64* sens, float mu, float lambda, float gamma,
+                        void* cuda_stream);
+
+/* Rebuild Lambda^{-1} from the context's sens/mask/weights (the preconditioner build of
+ * PAPER.md:238 / Table 2, timed by bench.py as part of a step). */
+sb_status sb_pcg_build_precond(sb_ctx* ctx);
+
+/* y = A x for all B problems.  x, y: complex [B][d0][d1]. */
+sb_status sb_pcg_apply_A(sb_ctx* ctx, const sb_c64* x, sb_c64* y);
+
+/* z = M^{-1} r = F^H diag{k}^{-1} F r.  r, z: complex [B][d0][d1]. */
+sb_status sb_pcg_apply_Pinv(sb_ctx* ctx, const sb_c64* r, sb_c64* z);
+
+/* y_c = R F S_c x (Eq. ill0); full != 0 replaces R by I.
+ * x: complex [B][d0][d1]; y: complex [B][C][d0][d1]. */
+sb_status sb_encode(sb_ctx* ctx, const sb_c64* x, sb_c64* y, int32_t full);
+
+/* x = sum_c S_c^H F^H R y_c (first term of b without mu).
+ * y: complex [B][C][d0][d1]; x: complex [B][d0][d1]. */
+sb_status sb_adjoint(sb_ctx* ctx, const sb_c64* y, sb_c64* x);
+
+typedef struct {
+  float eps;          /* stop when ||r_k||/||b|| <= eps; 0 => fixed count   */
+  int32_t max_iters;  /* >= 1                                                              */
+  int32_t precond;    /* 0 none, 1 circulant                                */
+  int32_t use_graph;  /* 1: device-driven loop in a CUDA graph (conditional while node)   */
+} sb_pcg_opts;
+
+typedef struct {      /* host arrays (NULL = not requested)                                */
+  int32_t* iters;     /* [B] A p products in the loop (reading A16)                        */
+  float* final_relres;/* [B] ||r_k|| / ||b|| (recurrence residual, reading A15)            */
+  int8_t* converged;  /* [B]                                                               */
+  float* relres_hist; /* [B][max_iters + 1]; entries past iters[b] are undefined           */
+} sb_pcg_stats;
+
+/* Solve A x = b by PCG for all B problems; x holds x0 on entry
+ * and the solution on exit.  Reaching max_iters is not an error (converged = 0 when
+ * eps > 0).  ||b|| = 0 returns x = 0, converged.  Errors: SB_E_INDEFINITE,
+ * SB_E_NONFINITE (first failing problem's status), SB_E_ARG. */
+sb_status sb_pcg_solve(sb_ctx* ctx, const sb_c64* b, sb_c64* x, const sb_pcg_opts* opts,
+                       sb_pcg_stats* stats);
+
+typedef struct {
+  int32_t n_outer, n_inner;  /* Algorithm 1 loops; n_inner must be 1 */
+  sb_pcg_opts pcg;
+} sb_recon_opts;
+
+typedef struct {             /* host outputs (NULL members = not requested)               */
+  int32_t* pcg_iters;        /* [n_outer * n_inner][B]                                    */
+  float* final_relres;       /* [n_outer * n_inner][B]                                    */
+  double total_ms;           /* device time of the whole call (CUDA events)               */
+} sb_recon_log;
+
+/* Split Bregman reconstruction, Algorithm 1 with per-problem PCG.
+ *   y      complex [B][C][d0][d1] zero-filled k-space
+ *   x_out  complex [B][d0][d1] reconstruction
+ * Step 1 x = RSS(F^H y_c) (reading A12); steps 6-11 with literal thresholds 1/lambda,
+ * 1/gamma (reading A8); data feedback (steps 13-15) in the exact image-domain form
+ * u_{j+1} = u_j + u_1 - E^H E x. */
+sb_status sb_recon(sb_ctx* ctx, const sb_c64* y, const sb_recon_opts* opts, sb_c64* x_out,
+                   sb_recon_log* log);
+
+/* One SB shrink/Bregman step (Alg. 1 steps 6-11) plus the regulariser part of the next
+ * RHS (step 4): given x and b_x, b_y, b_w (complex [B][d0][d1] each, b_w in the Haar
+ * Mallat layout), writes the updated b_x, b_y, b_w and
+ *   rhs_reg = lambda sum_d D_d^H (d_d - b_d) + gamma W^H (d_w - b_w).
+ * In-place on b_* is allowed (the only aliasing allowed by the ABI). */
+sb_status sb_sb_update(sb_ctx* ctx, const sb_c64* x, sb_c64* bx, sb_c64* by, sb_c64* bw,
+                       sb_c64* rhs_reg);
+
+/* Real k (not 1/(N k)) as built, fp64 [B or 1][d0][d1] — parity output. */
+sb_status sb_pcg_get_k(sb_ctx* ctx, double* k_out);
+
+/* Kernel timing for bench.py's roofline: when enabled, CUDA events bracket every launch
+ * of the matvec kernel (K1) on the context's stream and sb_get_kernel_time returns the
+ * accumulated device ms, launch count, and the algorithmic bytes per launch. */
+sb_status sb_set_kernel_timing(sb_ctx* ctx, int32_t enable);
+sb_status sb_get_kernel_time(sb_ctx* ctx, int32_t which /*0 = matvec K1, 1 = precond K2*/,
+                             double* ms, int64_t* launches, double* alg_bytes_per_launch);
+
+/* Number of kernels launched by this context since creation (for bench.py). */
+int64_t sb_kernel_launch_count(const sb_ctx* ctx);
+
+void sb_pcg_destroy(sb_ctx* ctx);
+const char* sb_status_str(sb_status s);
+const char* sb_last_error(const sb_ctx* ctx);
+int32_t sb_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SBPCG_H */

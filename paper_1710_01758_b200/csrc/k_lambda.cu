@@ -1,0 +1,223 @@
+// k_lambda.cu — K4: build of the circulant preconditioner's diagonal, in fp64 on the device
+// (reading A5), once per context ("constructed beforehand").
+//
+//   k = mu k_c + lambda k_d + gamma k_w              (Eq. Kdiag)
+//   k_c(nu) = sum_q g(q) r(nu + q),  g = sum_c |D s_c|^2 / N^2      (PAPER.md:199-229,
+//             the circular correlation form of Eq. diagonalelements; reading A2)
+//           = D^{-1}[ conj(D g) . D r ]            (D = unnormalised 2D DFT, g real)
+//   k_d(nu) = sum_d 4 sin^2(pi nu_d / n_d)         (eigenvalues of t_1)
+//   k_w = 1
+// Outputs k (fp64, parity) and Lambda^{-1} = 1/(N k) (fp32; the 1/N of the unnormalised
+// inverse FFT used by the preconditioner kernels is folded in).
+// FLOPs (Table 1): C forward 2D FFTs of the coil maps plus 3 FFTs.
+#include "kernels.cuh"
+
+namespace sbk {
+
+enum LKind {
+  L_COL_SENS = 0,   // tmp[b][c] = colFFT(sens[b][c])
+  L_ROW_ACC = 1,    // g[b][k0][k1] = sum_c |rowFFT(tmp[b][c])|^2 / N^2
+  L_COL_G = 2,      // g[b] = colFFT(g[b])           (in place)
+  L_ROW_G = 3,      // g[b] = rowFFT(g[b])           (in place)
+  L_COL_MASK = 4,   // rhat[m] = colFFT(mask[m])
+  L_ROW_MASK = 5,   // rhat[m] = rowFFT(rhat[m])     (in place)
+  L_ROW_PROD = 6,   // g[b] = rowIFFT(conj(g[b]) . rhat[mask(b)])
+  L_COL_FINAL = 7,  // k_c = colIFFT(g[b]) / N ; k ; Lambda^{-1}
+};
+
+constexpr int LW = 8;  // columns per CTA
+
+template <int M>
+struct LCol {
+  static constexpr int N1 = Split<M>::N1, N2 = Split<M>::N2, NT = N2 * LW;
+  using Lay = typename ColLayout<M, LW>::L;
+  static constexpr int XS = ColLayout<M, LW>::size;
+};
+template <int N>
+struct LRow {
+  static constexpr int N1 = Split<N>::N1, N2 = Split<N>::N2;
+  static constexpr int LINES = (128 / N2) > 0 ? (128 / N2) : 1;
+  static constexpr int NT = LINES * N2;
+  using Lay = typename RowLayout<N, LINES>::L;
+  static constexpr int XS = RowLayout<N, LINES>::size;
+};
+
+template <int M, int KIND>
+__global__ void __launch_bounds__(LCol<M>::NT) k_lcol(const LamArgs a) {
+  using C = LCol<M>;
+  constexpr int N1 = C::N1;
+  __shared__ __align__(16) double2 xch[C::XS];
+  __shared__ double2 tw[M];
+  const int tid = threadIdx.x, j = tid / LW, l = tid % LW;
+  const int N = a.N;
+  const int col = blockIdx.x * LW + l;
+  const size_t img = (size_t)M * N;
+  for (int i = tid; i < M; i += C::NT) tw[i] = a.tw_m[i];
+  __syncthreads();
+  double2 v[N1];
+  if constexpr (KIND == L_COL_SENS) {
+    const int bc = blockIdx.y;  // b*C + c
+    const float2* s = a.sens + (size_t)bc * img;
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const float2 f = s[(size_t)natidx<M>(j, n1) * N + col];
+      v[n1] = make_double2(f.x, f.y);
+    }
+    fft_fwd<M, typename C::Lay>(v, xch, tw, j, l);
+    double2* t = a.tmp + (size_t)bc * img;
+#pragma unroll
+    for (int q = 0; q < N1; ++q) t[(size_t)specidx<M>(j, q) * N + col] = v[q];
+  } else if constexpr (KIND == L_COL_G || KIND == L_COL_MASK) {
+    const int bi = blockIdx.y;
+    double2* t = (KIND == L_COL_G ? a.g : a.rhat) + (size_t)bi * img;
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const size_t gi = (size_t)natidx<M>(j, n1) * N + col;
+      if constexpr (KIND == L_COL_G) {
+        v[n1] = t[gi];
+      } else {
+        v[n1] = make_double2(a.mask[(size_t)bi * a.mask_bstride + gi] ? 1.0 : 0.0, 0.0);
+      }
+    }
+    __syncthreads();
+    fft_fwd<M, typename C::Lay>(v, xch, tw, j, l);
+#pragma unroll
+    for (int q = 0; q < N1; ++q) t[(size_t)specidx<M>(j, q) * N + col] = v[q];
+  } else if constexpr (KIND == L_COL_FINAL) {
+    const int b = blockIdx.y;
+    const double2* t = a.g + (size_t)b * img;
+#pragma unroll
+    for (int q = 0; q < N1; ++q) v[q] = t[(size_t)specidx<M>(j, q) * N + col];
+    fft_inv<M, typename C::Lay>(v, xch, tw, j, l);
+    const double invN = 1.0 / (double)img;
+    const double PI = 3.14159265358979323846;
+    const double sc = sin(PI * (double)col / (double)N);
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const int row = natidx<M>(j, n1);
+      const double kc = v[n1].x * invN;  // k_c is real (Hermitian K)
+      const double sr = sin(PI * (double)row / (double)M);
+      const double kd = 4.0 * sr * sr + 4.0 * sc * sc;
+      const double k = a.mu * kc + a.lam * kd + a.gam;
+      const size_t gi = (size_t)b * img + (size_t)row * N + col;
+      a.k_out[gi] = k;
+      if (!(fabs(k) > 1e-14) || !isfinite(k)) atomicExch(a.bad, 1);
+      a.lam_inv[gi] = (float)(1.0 / ((double)img * k));
+    }
+  }
+}
+
+template <int N, int KIND>
+__global__ void __launch_bounds__(LRow<N>::NT) k_lrow(const LamArgs a) {
+  using R = LRow<N>;
+  constexpr int N1 = R::N1, N2 = R::N2, LINES = R::LINES;
+  __shared__ __align__(16) double2 xch[R::XS];
+  __shared__ double2 tw[N];
+  const int tid = threadIdx.x, line = tid / N2, j = tid % N2;
+  const int M = a.M;
+  const int row0 = blockIdx.x * LINES + line;
+  const bool in_range = row0 < M;
+  const int row = in_range ? row0 : M - 1;
+  const size_t img = (size_t)M * N;
+  for (int i = tid; i < N; i += R::NT) tw[i] = a.tw_n[i];
+  __syncthreads();
+  double2 v[N1];
+  if constexpr (KIND == L_ROW_ACC) {
+    const int b = blockIdx.y;
+    double acc[N1];
+#pragma unroll
+    for (int s = 0; s < N1; ++s) acc[s] = 0.0;
+    for (int c = 0; c < a.C; ++c) {
+      const double2* t = a.tmp + ((size_t)b * a.C + c) * img + (size_t)row * N;
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) v[n1] = t[natidx<N>(j, n1)];
+      fft_fwd<N, typename R::Lay>(v, xch, tw, j, line);
+#pragma unroll
+      for (int s = 0; s < N1; ++s) acc[s] += v[s].x * v[s].x + v[s].y * v[s].y;
+      __syncthreads();
+    }
+    const double inv = 1.0 / ((double)img * (double)img);
+    if (in_range) {
+      double2* g = a.g + (size_t)b * img + (size_t)row * N;
+#pragma unroll
+      for (int s = 0; s < N1; ++s) g[specidx<N>(j, s)] = make_double2(acc[s] * inv, 0.0);
+    }
+  } else if constexpr (KIND == L_ROW_G || KIND == L_ROW_MASK) {
+    double2* t = (KIND == L_ROW_G ? a.g : a.rhat) + (size_t)blockIdx.y * img + (size_t)row * N;
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) v[n1] = t[natidx<N>(j, n1)];
+    __syncthreads();
+    fft_fwd<N, typename R::Lay>(v, xch, tw, j, line);
+    if (in_range) {
+#pragma unroll
+      for (int s = 0; s < N1; ++s) t[specidx<N>(j, s)] = v[s];
+    }
+  } else if constexpr (KIND == L_ROW_PROD) {
+    const int b = blockIdx.y;
+    const int m = (a.nmask == 1) ? 0 : b;
+    double2* t = a.g + (size_t)b * img + (size_t)row * N;
+    const double2* rh = a.rhat + (size_t)m * img + (size_t)row * N;
+#pragma unroll
+    for (int s = 0; s < N1; ++s) {
+      const int k = specidx<N>(j, s);
+      v[s] = cmulc(t[k], rh[k]);  // conj(D g) . D r
+    }
+    __syncthreads();
+    fft_inv<N, typename R::Lay>(v, xch, tw, j, line);
+    if (in_range) {
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) t[natidx<N>(j, n1)] = v[n1];
+    }
+  }
+}
+
+template <int M, int KIND>
+static cudaError_t lcol(const LamArgs& a, int nimg, cudaStream_t st) {
+  k_lcol<M, KIND><<<dim3(a.N / LW, nimg), LCol<M>::NT, 0, st>>>(a);
+  return cudaGetLastError();
+}
+template <int N, int KIND>
+static cudaError_t lrow(const LamArgs& a, int nimg, cudaStream_t st) {
+  k_lrow<N, KIND><<<dim3((a.M + LRow<N>::LINES - 1) / LRow<N>::LINES, nimg), LRow<N>::NT, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int M, int N>
+static cudaError_t build_mn(const LamArgs& a, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = lcol<M, L_COL_SENS>(a, a.B * a.C, st))) return e;
+  if ((e = lrow<N, L_ROW_ACC>(a, a.B, st))) return e;
+  if ((e = lcol<M, L_COL_G>(a, a.B, st))) return e;
+  if ((e = lrow<N, L_ROW_G>(a, a.B, st))) return e;
+  if ((e = lcol<M, L_COL_MASK>(a, a.nmask, st))) return e;
+  if ((e = lrow<N, L_ROW_MASK>(a, a.nmask, st))) return e;
+  if ((e = lrow<N, L_ROW_PROD>(a, a.B, st))) return e;
+  return lcol<M, L_COL_FINAL>(a, a.B, st);
+}
+
+template <int M>
+static cudaError_t build_m(const LamArgs& a, cudaStream_t st) {
+  switch (a.N) {
+    case 8: return build_mn<M, 8>(a, st);
+    case 16: return build_mn<M, 16>(a, st);
+    case 32: return build_mn<M, 32>(a, st);
+    case 64: return build_mn<M, 64>(a, st);
+    case 128: return build_mn<M, 128>(a, st);
+    case 256: return build_mn<M, 256>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_lambda_build(const LamArgs& a, cudaStream_t st) {
+  switch (a.M) {
+    case 8: return build_m<8>(a, st);
+    case 16: return build_m<16>(a, st);
+    case 32: return build_m<32>(a, st);
+    case 64: return build_m<64>(a, st);
+    case 128: return build_m<128>(a, st);
+    case 256: return build_m<256>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace sbk

@@ -1,0 +1,336 @@
+// k_matvec.cu — K1: the fused system-matrix application q = A p,
+//
+//   A p = mu sum_c conj(s_c) . F^H( r . F(s_c . p) ) + lambda L p + gamma p,
+//
+// L = D_x^H D_x + D_y^H D_y (periodic 5-point Laplacian) and
+// gamma W^H W = gamma I.  One CTA owns one column tile (all M = d0 rows x W
+// columns) of one problem.
+//
+// Separable (line) masks (r depends on the d0 row only): with F = F_0 (x) F_1
+// the data term is exactly  F_0^H R_0 F_0 (x) I  per coil, so each coil needs one length-M
+// FFT pair down every column, scaled by r/M.
+// Generic masks: passes A/B (k_passes.cu) leave r . F(s_c p) transformed along d1 back to
+// the (k0, n1) domain in tmpc, and this kernel only does the column IFFT.
+//
+// Per coil: the s_c tile (M x W complex64) arrives by 3D TMA into a 2-stage ring (mbarrier
+// complete_tx); the column FFT is register resident (four-step, fft_core.cuh); the coil
+// sum accumulates in registers.  G CTAs of a thread-block cluster split the coils and
+// reduce their partial sums through DSMEM in a fixed order (deterministic), then each
+// finishes M/G rows of the epilogue.
+#include <cooperative_groups.h>
+
+#include "kernels.cuh"
+#include "pcg_fin.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace sbk {
+
+template <int M, int W, int MODE, bool SEP>
+__global__ void __launch_bounds__(Split<M>::N2* W)
+    k1_matvec(const __grid_constant__ CUtensorMap tmap, const K1Args a) {
+  constexpr int N1 = Split<M>::N1, N2 = Split<M>::N2;
+  constexpr int NT = N2 * W;
+  constexpr int TILE = M * W;          // complex elements per tile
+  constexpr int PW = W + 2;            // p tile with +-1 column halo
+  using Lay = typename ColLayout<M, W>::L;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float2* ring = reinterpret_cast<float2*>(smem_raw);                 // [2][TILE]
+  float2* xch = ring + 2 * TILE;                                     // ColLayout size
+  float2* pt = xch + ColLayout<M, W>::size;                          // [M][PW]
+  float2* tw = pt + M * PW;                                          // [M]
+  float* rm = reinterpret_cast<float*>(tw + M);                      // [M]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(rm + M + (M & 1));     // [2]
+  __shared__ double red[32];
+  __shared__ int lastflag;
+
+  const int G = gridDim.x;
+  const int g = blockIdx.x;
+  const int tile = blockIdx.y;
+  const int b = blockIdx.z;
+  const int tid = threadIdx.x;
+  const int j = tid / W, l = tid % W;
+  const int col0 = tile * W;
+  const int N = a.N;
+  const size_t img = (size_t)M * N;
+  const size_t boff = (size_t)b * img;
+
+  int pidx = 0;
+  double beta = 0.0, alpha_prev = 0.0;
+  bool first = true;
+  if constexpr (MODE == K1_PCG) {
+    const Scal& s = a.L.scal[b];
+    if (!s.active) return;  // uniform over the cluster (same problem)
+    const int k = s.iter + 1;  // iteration being formed
+    first = (k == 1);
+    pidx = k & 1;
+    beta = s.beta;
+    alpha_prev = s.alpha;
+  }
+
+  // ---- setup: barriers, twiddles, mask
+  const int ncoil = (a.C - g + G - 1) / G;  // coils g, g+G, ...
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < M; i += NT) {
+    tw[i] = a.tw[i];
+    if constexpr (SEP) rm[i] = a.rmask[(size_t)b * a.rmask_bstride + i];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < 2 && s < ncoil; ++s) {
+      const int c = g + s * G;
+      mbar_expect_tx(&bar[s], TILE * 8);
+      tma_load_3d(ring + s * TILE, &tmap, 2 * col0, 0, b * a.C + c, &bar[s]);
+    }
+  }
+
+  // ---- prologue: the p tile (+halo); PCG forms p_k = z + beta p_{k-1} and x += alpha p_{k-1}
+  const int rows_per = M / G;
+  const int r0 = g * rows_per, r1 = r0 + rows_per;
+  for (int e = tid; e < M * PW; e += NT) {
+    const int row = e / PW, cc = e % PW;
+    const int gcol = (col0 + cc - 1 + N) % N;
+    const size_t gi = boff + (size_t)row * N + gcol;
+    float2 p;
+    if constexpr (MODE == K1_PCG) {
+      const float2 zz = a.z[gi];
+      if (first) {
+        p = zz;
+      } else {
+        const float2* pold = pidx ? a.pbuf0 : a.pbuf1;
+        const float2 po = pold[gi];
+        p = make_float2(zz.x + (float)beta * po.x, zz.y + (float)beta * po.y);
+        if (cc >= 1 && cc <= W && row >= r0 && row < r1) {
+          float2 xv = a.x[gi];
+          xv.x += (float)alpha_prev * po.x;
+          xv.y += (float)alpha_prev * po.y;
+          a.x[gi] = xv;
+        }
+      }
+      if (cc >= 1 && cc <= W && row >= r0 && row < r1) (pidx ? a.pbuf1 : a.pbuf0)[gi] = p;
+    } else {
+      p = a.vin[gi];
+    }
+    pt[e] = p;
+  }
+  __syncthreads();
+
+  // ---- coil loop
+  float2 acc[N1];
+#pragma unroll
+  for (int i = 0; i < N1; ++i) acc[i] = make_float2(0.f, 0.f);
+
+  for (int ci = 0; ci < ncoil; ++ci) {
+    const int stage = ci & 1;
+    mbar_wait(&bar[stage], (ci >> 1) & 1);
+    const float2* sc = ring + stage * TILE;
+    float2 s[N1], v[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const int row = natidx<M>(j, n1);
+      s[n1] = sc[row * W + l];
+    }
+    if constexpr (SEP) {
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) {
+        const int row = natidx<M>(j, n1);
+        v[n1] = cmul(s[n1], pt[row * PW + l + 1]);
+      }
+      fft_fwd<M, Lay>(v, xch, tw, j, l);
+      // every thread has read ring[stage] before the barrier inside fft_fwd
+      if (tid == 0 && ci + 2 < ncoil) {
+        const int c = g + (ci + 2) * G;
+        mbar_expect_tx(&bar[stage], TILE * 8);
+        tma_load_3d(ring + stage * TILE, &tmap, 2 * col0, 0, b * a.C + c, &bar[stage]);
+      }
+#pragma unroll
+      for (int q = 0; q < N1; ++q) {
+        const float r = rm[specidx<M>(j, q)];
+        v[q] = make_float2(v[q].x * r, v[q].y * r);
+      }
+    } else {
+      const int c = g + ci * G;
+      const float2* tc = a.tmpc + ((size_t)b * a.C + c) * img;
+#pragma unroll
+      for (int q = 0; q < N1; ++q) v[q] = tc[(size_t)specidx<M>(j, q) * N + col0 + l];
+      __syncthreads();  // all threads read ring[stage]
+      if (tid == 0 && ci + 2 < ncoil) {
+        const int c2 = g + (ci + 2) * G;
+        mbar_expect_tx(&bar[stage], TILE * 8);
+        tma_load_3d(ring + stage * TILE, &tmap, 2 * col0, 0, b * a.C + c2, &bar[stage]);
+      }
+    }
+    fft_inv<M, Lay>(v, xch, tw, j, l);
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const float2 t = cmulc(s[n1], v[n1]);
+      acc[n1].x += t.x;
+      acc[n1].y += t.y;
+    }
+    if constexpr (!SEP) __syncthreads();  // xch reuse between consecutive inverses
+  }
+
+  // ---- coil-group reduction (DSMEM) + epilogue
+  __syncthreads();
+  float2* accb = ring;  // TILE elements; the ring is drained
+#pragma unroll
+  for (int n1 = 0; n1 < N1; ++n1) accb[natidx<M>(j, n1) * W + l] = acc[n1];
+  cg::cluster_group cluster = cg::this_cluster();
+  if (G > 1) cluster.sync(); else __syncthreads();
+
+  double d0 = 0.0, d1 = 0.0;
+  for (int e = tid; e < rows_per * W; e += NT) {
+    const int row = r0 + e / W, cc = e % W;
+    float2 av = make_float2(0.f, 0.f);
+    for (int gg = 0; gg < G; ++gg) {
+      const float2* src = (gg == g) ? accb : cluster.map_shared_rank(accb, gg);
+      const float2 t = src[row * W + cc];
+      av.x += t.x;
+      av.y += t.y;
+    }
+    const float2 p = pt[row * PW + cc + 1];
+    const float2 pu = pt[((row + M - 1) % M) * PW + cc + 1];
+    const float2 pd = pt[((row + 1) % M) * PW + cc + 1];
+    const float2 pl = pt[row * PW + cc];
+    const float2 pr = pt[row * PW + cc + 2];
+    const float2 lp = make_float2(4.f * p.x - pu.x - pd.x - pl.x - pr.x,
+                                  4.f * p.y - pu.y - pd.y - pl.y - pr.y);
+    const size_t gi = boff + (size_t)row * N + col0 + cc;
+    const float2 reg = make_float2(a.lam * lp.x + a.gam * p.x, a.lam * lp.y + a.gam * p.y);
+    if constexpr (MODE == K1_RESID) {
+      float2 bb;
+      if (a.bvec != nullptr) {
+        bb = a.bvec[gi];
+      } else {
+        float2 uu = a.u[gi];
+        if (a.update_u) {
+          const float2 u1 = a.u1[gi];
+          uu = make_float2(uu.x + u1.x - av.x, uu.y + u1.y - av.y);
+          a.u[gi] = uu;
+        }
+        bb = make_float2(a.mu * uu.x, a.mu * uu.y);
+        if (a.rhs_reg != nullptr) {
+          const float2 rr = a.rhs_reg[gi];
+          bb.x += rr.x;
+          bb.y += rr.y;
+        }
+        a.bout[gi] = bb;
+      }
+      const float2 r = make_float2(bb.x - (a.mu * av.x + reg.x), bb.y - (a.mu * av.y + reg.y));
+      a.out[gi] = r;
+      d0 += (double)bb.x * bb.x + (double)bb.y * bb.y;
+      d1 += (double)r.x * r.x + (double)r.y * r.y;
+    } else {
+      const float2 q = make_float2(a.mu * av.x + reg.x, a.mu * av.y + reg.y);
+      a.out[gi] = q;
+      d0 += (double)p.x * q.x + (double)p.y * q.y;
+    }
+  }
+  if (G > 1) cluster.sync();  // peers finished reading this CTA's accb
+
+  if constexpr (MODE == K1_APPLY) return;
+  const double s0 = block_sum(d0, red);
+  double s1 = 0.0;
+  if constexpr (MODE == K1_RESID) s1 = block_sum(d1, red);
+  const int nblk = gridDim.x * gridDim.y;
+  const bool last = publish_and_check_last(s0, s1, a.P, b, tile * G + g, nblk, &lastflag);
+  if (!last) return;
+  if (tid < 32) {
+    const double t0 = warp_sum_partials(a.P.p0 + (size_t)b * a.P.cap, nblk);
+    double t1 = 0.0;
+    if constexpr (MODE == K1_RESID) t1 = warp_sum_partials(a.P.p1 + (size_t)b * a.P.cap, nblk);
+    if (tid == 0) {
+      if constexpr (MODE == K1_PCG) fin_sigma(a.L, b, t0);
+      else fin_init(a.L, b, t0, t1, a.eps, a.maxit);
+      a.P.cnt[b] = 0;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host launchers
+template <int M, int W>
+constexpr size_t k1_smem() {
+  return (size_t)(2 * M * W + ColLayout<M, W>::size + M * (W + 2) + M) * sizeof(float2) +
+         (M + (M & 1)) * sizeof(float) + 2 * sizeof(uint64_t);
+}
+
+template <int M, int W, int MODE, bool SEP>
+static cudaError_t launch_k1_t(const K1Args& a, const CUtensorMap* tmap, int G, cudaStream_t st) {
+  auto kern = k1_matvec<M, W, MODE, SEP>;
+  constexpr size_t smem = k1_smem<M, W>();
+  static bool attr_done = false;  // per instantiation
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G, a.N / W, a.B);
+  cfg.blockDim = dim3(Split<M>::N2 * W);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, *tmap, a);
+}
+
+template <int M, int W>
+static cudaError_t launch_k1_mw(int mode, bool sep, const K1Args& a, const CUtensorMap* tmap, int G,
+                                cudaStream_t st) {
+  if (sep) {
+    switch (mode) {
+      case K1_APPLY: return launch_k1_t<M, W, K1_APPLY, true>(a, tmap, G, st);
+      case K1_PCG: return launch_k1_t<M, W, K1_PCG, true>(a, tmap, G, st);
+      default: return launch_k1_t<M, W, K1_RESID, true>(a, tmap, G, st);
+    }
+  } else {
+    switch (mode) {
+      case K1_APPLY: return launch_k1_t<M, W, K1_APPLY, false>(a, tmap, G, st);
+      case K1_PCG: return launch_k1_t<M, W, K1_PCG, false>(a, tmap, G, st);
+      default: return launch_k1_t<M, W, K1_RESID, false>(a, tmap, G, st);
+    }
+  }
+}
+
+template <int M>
+static cudaError_t launch_k1_m(int mode, bool sep, const K1Args& a, const CUtensorMap* tmap, int W, int G,
+                               cudaStream_t st) {
+  switch (W) {
+    case 4: return launch_k1_mw<M, 4>(mode, sep, a, tmap, G, st);
+    case 8: return launch_k1_mw<M, 8>(mode, sep, a, tmap, G, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+bool k1_supported(int M, int N) {
+  const bool m_ok = (M == 8 || M == 16 || M == 32 || M == 64 || M == 128 || M == 256);
+  return m_ok && N >= 4 && N % 4 == 0 && N <= 65536;
+}
+
+int k1_default_W(int M, int N) { return (N % 8 == 0) ? 8 : 4; }
+
+cudaError_t launch_k1(int mode, bool separable, const K1Args& a, const CUtensorMap* tmap, int W, int G,
+                      cudaStream_t st) {
+  if (a.M % G != 0 || a.N % W != 0) return cudaErrorInvalidValue;
+  switch (a.M) {
+    case 8: return launch_k1_m<8>(mode, separable, a, tmap, W, G, st);
+    case 16: return launch_k1_m<16>(mode, separable, a, tmap, W, G, st);
+    case 32: return launch_k1_m<32>(mode, separable, a, tmap, W, G, st);
+    case 64: return launch_k1_m<64>(mode, separable, a, tmap, W, G, st);
+    case 128: return launch_k1_m<128>(mode, separable, a, tmap, W, G, st);
+    case 256: return launch_k1_m<256>(mode, separable, a, tmap, W, G, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace sbk

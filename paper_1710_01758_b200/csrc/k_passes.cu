@@ -1,0 +1,460 @@
+// k_passes.cu — column / row FFT passes (fp32) used by
+//   * the circulant preconditioner  z = F^H diag{k}^{-1} F r, split in
+//     K2a (column FFT, fused r -= alpha q and ||r||^2), K2b (row FFT, x Lambda^{-1}, row
+//     IFFT), K2c (column IFFT, fused <r, z>) — Lambda^{-1} = 1/(N k) folds the 1/N;
+//   * the encoding operator E_c = R F S_c and its adjoint (Alg. 1 step 4);
+//   * SB init: u_1 = sum_c S_c^H F^H y_c and x^[1] = RSS (reading A12);
+//   * generic (non-separable mask) matvec passes A and B;
+//   * the no-preconditioner step and the PCG exit fixup.
+// Column passes: one CTA = W columns x all M rows of one image, threads (j, col) with col
+// fastest (coalesced rows of W*8 bytes).  Row passes: one CTA = LINES rows, threads
+// (line, j) with j fastest.  Each transform is the four-step register FFT of fft_core.cuh.
+#include "kernels.cuh"
+#include "pcg_fin.cuh"
+
+namespace sbk {
+
+constexpr int PW_COL = 8;  // columns per column-pass CTA
+
+template <int M>
+struct ColCfg {
+  static constexpr int W = PW_COL;
+  static constexpr int N1 = Split<M>::N1, N2 = Split<M>::N2, NT = N2 * W;
+  using Lay = typename ColLayout<M, W>::L;
+  static constexpr int XS = ColLayout<M, W>::size;
+};
+
+template <int N>
+struct RowCfg {
+  static constexpr int N1 = Split<N>::N1, N2 = Split<N>::N2;
+  static constexpr int LINES = (256 / N2) > 0 ? (256 / N2) : 1;
+  static constexpr int NT = LINES * N2;
+  using Lay = typename RowLayout<N, LINES>::L;
+  static constexpr int XS = RowLayout<N, LINES>::size;
+};
+
+__device__ __forceinline__ bool slice_active(const PassArgs& a, int b) {
+  return a.L.scal == nullptr || __ldcg(&a.L.scal[b].active) != 0;
+}
+
+// ------------------------------------------------------------------ column passes
+template <int M, int KIND>
+__global__ void __launch_bounds__(ColCfg<M>::NT) k_col(const PassArgs a) {
+  using C = ColCfg<M>;
+  constexpr int N1 = C::N1, W = C::W, NT = C::NT;
+  __shared__ __align__(16) float2 xch[C::XS];
+  __shared__ float2 tw[M];
+  __shared__ double red[32];
+  __shared__ int lastflag;
+  const int tid = threadIdx.x, j = tid / W, l = tid % W;
+  const int N = a.N;
+  const int col = blockIdx.x * W + l;
+  const size_t img = (size_t)M * N;
+
+  // image / problem index
+  int b, c = 0;
+  if constexpr (KIND == P_ENC_COL || KIND == P_GEN_A_COL) {
+    b = blockIdx.y / a.C;
+    c = blockIdx.y % a.C;
+  } else {
+    b = blockIdx.y;
+  }
+  const size_t boff = (size_t)b * img;
+
+  if constexpr (KIND == P_PRE_A_FWD_COL || KIND == P_PRE_C_INV_COL || KIND == P_GEN_A_COL) {
+    if (!slice_active(a, b)) {
+      if constexpr (KIND == P_PRE_C_INV_COL) {
+        if (a.L.scal != nullptr && a.mode >= 0 && blockIdx.x == 0 && tid == 0) slice_arrive(a.L);
+      }
+      return;
+    }
+  }
+  for (int i = tid; i < M; i += NT) tw[i] = a.tw_m[i];
+  __syncthreads();
+
+  float2 v[N1];
+  double d0 = 0.0;
+
+  if constexpr (KIND == P_PRE_A_FWD_COL) {
+    // mode 1 (PCG): r_k = r_{k-1} - alpha_k q_k ; mode 0 (init): r given
+    const double alpha = (a.mode == 1) ? a.L.scal[b].alpha : 0.0;
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const size_t gi = boff + (size_t)natidx<M>(j, n1) * N + col;
+      float2 r = a.a0[gi];
+      if (a.mode == 1) {
+        const float2 q = a.a1[gi];
+        r.x -= (float)alpha * q.x;
+        r.y -= (float)alpha * q.y;
+        a.o0[gi] = r;
+        d0 += (double)r.x * r.x + (double)r.y * r.y;
+      }
+      v[n1] = r;
+    }
+    fft_fwd<M, typename C::Lay>(v, xch, tw, j, l);
+#pragma unroll
+    for (int s = 0; s < N1; ++s) a.tmp[boff + (size_t)specidx<M>(j, s) * N + col] = v[s];
+    if (a.mode == 1) {
+      const double s0 = block_sum(d0, red);
+      const int nblk = gridDim.x;
+      if (publish_and_check_last(s0, 0.0, a.P, b, blockIdx.x, nblk, &lastflag)) {
+        if (tid < 32) {
+          const double t = warp_sum_partials(a.P.p0 + (size_t)b * a.P.cap, nblk);
+          if (tid == 0) {
+            fin_rr(a.L, b, t);
+            a.P.cnt[b] = 0;
+          }
+        }
+      }
+    }
+  } else if constexpr (KIND == P_PRE_C_INV_COL) {
+#pragma unroll
+    for (int s = 0; s < N1; ++s) v[s] = a.tmp[boff + (size_t)specidx<M>(j, s) * N + col];
+    fft_inv<M, typename C::Lay>(v, xch, tw, j, l);
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const size_t gi = boff + (size_t)natidx<M>(j, n1) * N + col;
+      a.o0[gi] = v[n1];
+      if (a.mode >= 0) {
+        const float2 r = a.a0[gi];
+        d0 += (double)r.x * v[n1].x + (double)r.y * v[n1].y;
+      }
+    }
+    if (a.mode >= 0) {
+      const double s0 = block_sum(d0, red);
+      const int nblk = gridDim.x;
+      if (publish_and_check_last(s0, 0.0, a.P, b, blockIdx.x, nblk, &lastflag)) {
+        if (tid < 32) {
+          const double t = warp_sum_partials(a.P.p0 + (size_t)b * a.P.cap, nblk);
+          if (tid == 0) {
+            fin_rho(a.L, b, t, a.mode == 0);
+            a.P.cnt[b] = 0;
+            slice_arrive(a.L);
+          }
+        }
+      }
+    }
+  } else if constexpr (KIND == P_ENC_COL || KIND == P_GEN_A_COL) {
+    const float2* sc = a.sens + ((size_t)b * a.C + c) * img;
+    const float2* pin = a.a0;
+    double beta = 0.0;
+    bool first = true;
+    int pidx = 0;
+    if constexpr (KIND == P_GEN_A_COL) {
+      if (a.mode == 1) {
+        const Scal& s = a.L.scal[b];
+        const int k = s.iter + 1;
+        first = (k == 1);
+        pidx = k & 1;
+        beta = s.beta;
+      }
+    }
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const size_t gi = boff + (size_t)natidx<M>(j, n1) * N + col;
+      float2 p;
+      if (KIND == P_GEN_A_COL && a.mode == 1) {
+        const float2 zz = a.z[gi];
+        if (first) {
+          p = zz;
+        } else {
+          const float2 po = (pidx ? a.pbuf0 : a.pbuf1)[gi];
+          p = make_float2(zz.x + (float)beta * po.x, zz.y + (float)beta * po.y);
+        }
+      } else {
+        p = pin[gi];
+      }
+      v[n1] = cmul(sc[gi - boff], p);
+    }
+    fft_fwd<M, typename C::Lay>(v, xch, tw, j, l);
+    float2* t = a.tmp + ((size_t)b * a.C + c) * img;
+#pragma unroll
+    for (int s = 0; s < N1; ++s) t[(size_t)specidx<M>(j, s) * N + col] = v[s];
+  } else if constexpr (KIND == P_ADJ_COL) {
+    float2 acc[N1];
+    float rss[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      acc[n1] = make_float2(0.f, 0.f);
+      rss[n1] = 0.f;
+    }
+    for (int cc = 0; cc < a.C; ++cc) {
+      const float2* t = a.tmp + ((size_t)b * a.C + cc) * img;
+      const float2* sc = a.sens + ((size_t)b * a.C + cc) * img;
+#pragma unroll
+      for (int s = 0; s < N1; ++s) v[s] = t[(size_t)specidx<M>(j, s) * N + col];
+      fft_inv<M, typename C::Lay>(v, xch, tw, j, l);
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) {
+        const float2 vv = make_float2(v[n1].x * a.scale, v[n1].y * a.scale);
+        const float2 s = sc[(size_t)natidx<M>(j, n1) * N + col];
+        const float2 u = cmulc(s, vv);
+        acc[n1].x += u.x;
+        acc[n1].y += u.y;
+        rss[n1] += vv.x * vv.x + vv.y * vv.y;
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const size_t gi = boff + (size_t)natidx<M>(j, n1) * N + col;
+      a.o0[gi] = acc[n1];
+      if (a.o1 != nullptr) a.o1[gi] = make_float2(sqrtf(rss[n1]), 0.f);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ row passes
+template <int N, int KIND>
+__global__ void __launch_bounds__(RowCfg<N>::NT) k_row(const PassArgs a) {
+  using R = RowCfg<N>;
+  constexpr int N1 = R::N1, N2 = R::N2, LINES = R::LINES, NT = R::NT;
+  __shared__ __align__(16) float2 xch[R::XS];
+  __shared__ float2 tw[N];
+  const int tid = threadIdx.x, line = tid / N2, j = tid % N2;
+  const int M = a.M;
+  const int row = blockIdx.x * LINES + line;
+  const size_t img = (size_t)M * N;
+  int b, c = 0;
+  if constexpr (KIND == P_PRE_B_ROW) {
+    b = blockIdx.y;
+    if (!slice_active(a, b)) return;
+  } else {
+    b = blockIdx.y / a.C;
+    c = blockIdx.y % a.C;
+    if constexpr (KIND == P_GEN_B_ROW) {
+      if (a.mode == 1 && !slice_active(a, b)) return;
+    }
+  }
+  for (int i = tid; i < N; i += NT) tw[i] = a.tw_n[i];
+  __syncthreads();
+  const bool in_range = row < M;
+  const int rr = in_range ? row : M - 1;  // keep barriers uniform
+  float2 v[N1];
+
+  if constexpr (KIND == P_PRE_B_ROW) {
+    float2* t = a.tmp + (size_t)b * img + (size_t)rr * N;
+    const float* li = a.lam_inv + (size_t)b * a.lam_bstride + (size_t)rr * N;
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) v[n1] = t[natidx<N>(j, n1)];
+    fft_fwd<N, typename R::Lay>(v, xch, tw, j, line);
+#pragma unroll
+    for (int s = 0; s < N1; ++s) {
+      const float f = li[specidx<N>(j, s)];
+      v[s] = make_float2(v[s].x * f, v[s].y * f);
+    }
+    fft_inv<N, typename R::Lay>(v, xch, tw, j, line);
+    if (in_range) {
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) t[natidx<N>(j, n1)] = v[n1];
+    }
+  } else if constexpr (KIND == P_GEN_B_ROW) {
+    float2* t = a.tmp + ((size_t)b * a.C + c) * img + (size_t)rr * N;
+    const uint8_t* mk = a.mask + (size_t)b * a.mask_bstride + (size_t)rr * N;
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) v[n1] = t[natidx<N>(j, n1)];
+    fft_fwd<N, typename R::Lay>(v, xch, tw, j, line);
+#pragma unroll
+    for (int s = 0; s < N1; ++s) {
+      const float f = mk[specidx<N>(j, s)] ? a.scale : 0.f;
+      v[s] = make_float2(v[s].x * f, v[s].y * f);
+    }
+    fft_inv<N, typename R::Lay>(v, xch, tw, j, line);
+    if (in_range) {
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) t[natidx<N>(j, n1)] = v[n1];
+    }
+  } else if constexpr (KIND == P_ENC_ROW) {
+    const float2* t = a.tmp + ((size_t)b * a.C + c) * img + (size_t)rr * N;
+    float2* y = a.o0 + ((size_t)b * a.C + c) * img + (size_t)rr * N;
+    const uint8_t* mk = a.mask + (size_t)b * a.mask_bstride + (size_t)rr * N;
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) v[n1] = t[natidx<N>(j, n1)];
+    fft_fwd<N, typename R::Lay>(v, xch, tw, j, line);
+    if (in_range) {
+#pragma unroll
+      for (int s = 0; s < N1; ++s) {
+        const int k = specidx<N>(j, s);
+        const float f = (a.full || mk[k]) ? a.scale : 0.f;
+        y[k] = make_float2(v[s].x * f, v[s].y * f);
+      }
+    }
+  } else if constexpr (KIND == P_ADJ_ROW) {
+    const float2* y = a.a0 + ((size_t)b * a.C + c) * img + (size_t)rr * N;
+    float2* t = a.tmp + ((size_t)b * a.C + c) * img + (size_t)rr * N;
+    const uint8_t* mk = a.mask + (size_t)b * a.mask_bstride + (size_t)rr * N;
+#pragma unroll
+    for (int s = 0; s < N1; ++s) {
+      const int k = specidx<N>(j, s);
+      const float2 yy = y[k];
+      v[s] = (a.full || mk[k]) ? yy : make_float2(0.f, 0.f);
+    }
+    fft_inv<N, typename R::Lay>(v, xch, tw, j, line);
+    if (in_range) {
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) t[natidx<N>(j, n1)] = v[n1];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ elementwise kernels
+// No preconditioner (precond = 0): r -= alpha q (PCG), z = r, rho' = ||r||^2.
+__global__ void __launch_bounds__(256) k_nopre(const PassArgs a) {
+  __shared__ double red[32];
+  __shared__ int lastflag;
+  const int b = blockIdx.y;
+  const size_t img = (size_t)a.M * a.N;
+  if (!slice_active(a, b)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) slice_arrive(a.L);
+    return;
+  }
+  const double alpha = (a.mode == 1) ? a.L.scal[b].alpha : 0.0;
+  double d0 = 0.0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < img; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t gi = (size_t)b * img + i;
+    float2 r = a.a0[gi];
+    if (a.mode == 1) {
+      const float2 q = a.a1[gi];
+      r.x -= (float)alpha * q.x;
+      r.y -= (float)alpha * q.y;
+      a.o0[gi] = r;
+    }
+    a.o1[gi] = r;  // z = r
+    d0 += (double)r.x * r.x + (double)r.y * r.y;
+  }
+  const double s0 = block_sum(d0, red);
+  const int nblk = gridDim.x;
+  if (publish_and_check_last(s0, 0.0, a.P, b, blockIdx.x, nblk, &lastflag)) {
+    if (threadIdx.x < 32) {
+      const double t = warp_sum_partials(a.P.p0 + (size_t)b * a.P.cap, nblk);
+      if (threadIdx.x == 0) {
+        if (a.mode == 1) {
+          fin_rr(a.L, b, t);
+          if (a.L.scal[b].active) fin_rho(a.L, b, t, false);
+        } else {
+          fin_rho(a.L, b, t, true);
+        }
+        a.P.cnt[b] = 0;
+        slice_arrive(a.L);
+      }
+    }
+  }
+}
+
+// PCG exit: x += alpha_K p_K (the last completed iteration), or x = 0 when ||b|| = 0.
+__global__ void __launch_bounds__(256) k_fixup(const PassArgs a) {
+  const int b = blockIdx.y;
+  const Scal& s = a.L.scal[b];
+  const size_t img = (size_t)a.M * a.N;
+  const int zero = s.zero_x;
+  const int K = s.iter;
+  const bool upd = (s.status == ST_OK) && (K >= 1);
+  if (!zero && !upd) return;
+  const float alpha = (float)s.alpha;
+  const float2* p = (K & 1) ? a.pbuf1 : a.pbuf0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < img; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t gi = (size_t)b * img + i;
+    if (zero) {
+      a.x[gi] = make_float2(0.f, 0.f);
+    } else {
+      float2 xv = a.x[gi];
+      const float2 pv = p[gi];
+      xv.x += alpha * pv.x;
+      xv.y += alpha * pv.y;
+      a.x[gi] = xv;
+    }
+  }
+}
+
+// Recon log row for this solve, then advance the solve index (one thread).
+__global__ void k_log(const Loop L) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int slot = L.ctl->solve_idx;
+  for (int b = 0; b < L.B; ++b) {
+    const Scal& s = L.scal[b];
+    if (L.log_iters) L.log_iters[(size_t)slot * L.B + b] = s.iter;
+    if (L.log_relres) L.log_relres[(size_t)slot * L.B + b] = (float)(s.nb2 > 0 ? sqrt(s.rr / s.nb2) : 0.0);
+  }
+  L.ctl->solve_idx = slot + 1;
+}
+
+cudaError_t launch_log(const Loop& L, cudaStream_t st) {
+  k_log<<<1, 32, 0, st>>>(L);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ dispatch
+template <int M, int KIND>
+static cudaError_t launch_col_t(const PassArgs& a, cudaStream_t st) {
+  int nimg = (KIND == P_ENC_COL || KIND == P_GEN_A_COL) ? a.B * a.C : a.B;
+  dim3 grid(a.N / PW_COL, nimg);
+  k_col<M, KIND><<<grid, ColCfg<M>::NT, 0, st>>>(a);
+  return cudaGetLastError();
+}
+template <int N, int KIND>
+static cudaError_t launch_row_t(const PassArgs& a, cudaStream_t st) {
+  int nimg = (KIND == P_PRE_B_ROW) ? a.B : a.B * a.C;
+  dim3 grid((a.M + RowCfg<N>::LINES - 1) / RowCfg<N>::LINES, nimg);
+  k_row<N, KIND><<<grid, RowCfg<N>::NT, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int KIND>
+static cudaError_t col_dispatch(const PassArgs& a, cudaStream_t st) {
+  switch (a.M) {
+    case 8: return launch_col_t<8, KIND>(a, st);
+    case 16: return launch_col_t<16, KIND>(a, st);
+    case 32: return launch_col_t<32, KIND>(a, st);
+    case 64: return launch_col_t<64, KIND>(a, st);
+    case 128: return launch_col_t<128, KIND>(a, st);
+    case 256: return launch_col_t<256, KIND>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+template <int KIND>
+static cudaError_t row_dispatch(const PassArgs& a, cudaStream_t st) {
+  switch (a.N) {
+    case 8: return launch_row_t<8, KIND>(a, st);
+    case 16: return launch_row_t<16, KIND>(a, st);
+    case 32: return launch_row_t<32, KIND>(a, st);
+    case 64: return launch_row_t<64, KIND>(a, st);
+    case 128: return launch_row_t<128, KIND>(a, st);
+    case 256: return launch_row_t<256, KIND>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+bool pass_supported(int M, int N) {
+  auto ok = [](int n) { return n == 8 || n == 16 || n == 32 || n == 64 || n == 128 || n == 256; };
+  return ok(M) && ok(N);
+}
+
+cudaError_t launch_pass(int kind, const PassArgs& a, cudaStream_t st) {
+  const size_t img = (size_t)a.M * a.N;
+  switch (kind) {
+    case P_PRE_A_FWD_COL: return col_dispatch<P_PRE_A_FWD_COL>(a, st);
+    case P_PRE_B_ROW: return row_dispatch<P_PRE_B_ROW>(a, st);
+    case P_PRE_C_INV_COL: return col_dispatch<P_PRE_C_INV_COL>(a, st);
+    case P_ENC_COL: return col_dispatch<P_ENC_COL>(a, st);
+    case P_ENC_ROW: return row_dispatch<P_ENC_ROW>(a, st);
+    case P_ADJ_ROW: return row_dispatch<P_ADJ_ROW>(a, st);
+    case P_ADJ_COL: return col_dispatch<P_ADJ_COL>(a, st);
+    case P_GEN_A_COL: return col_dispatch<P_GEN_A_COL>(a, st);
+    case P_GEN_B_ROW: return row_dispatch<P_GEN_B_ROW>(a, st);
+    case P_NOPRE: {
+      int nb = (int)((img + 2047) / 2048);
+      if (nb > 64) nb = 64;
+      k_nopre<<<dim3(nb, a.B), 256, 0, st>>>(a);
+      return cudaGetLastError();
+    }
+    case P_FIXUP: {
+      int nb = (int)((img + 1023) / 1024);
+      if (nb > 256) nb = 256;
+      k_fixup<<<dim3(nb, a.B), 256, 0, st>>>(a);
+      return cudaGetLastError();
+    }
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace sbk

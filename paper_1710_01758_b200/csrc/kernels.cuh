@@ -1,0 +1,128 @@
+// kernels.cuh — kernel argument structs and launcher declarations (internal).
+#pragma once
+#include "internal.cuh"
+
+namespace sbk {
+
+enum K1Mode { K1_APPLY = 0, K1_PCG = 1, K1_RESID = 2 };
+
+// Fused matvec q = A p for one column tile (all d0 rows x W columns)
+// of one problem; coil maps streamed by TMA; see k_matvec.cu.
+struct K1Args {
+  int B, C, M, N;
+  float mu, lam, gam;
+  const float* rmask;      // [B or 1][M] = r/M (separable) ; or null (generic)
+  int rmask_bstride;       // M or 0
+  const float2* tmpc;      // generic path: [B][C][M][N] spectra after pass B (layout: row = k0)
+  // APPLY: vin -> out = A vin.   RESID: vin = x, out = r.   PCG: out = q.
+  const float2* vin;
+  float2* out;
+  // PCG
+  const float2* z;
+  float2* pbuf0;
+  float2* pbuf1;
+  float2* x;
+  // RESID
+  const float2* bvec;      // given b (solve); null in recon mode
+  float2* u;               // recon: running u_j = sum_c E_c^H y_c^[j]
+  const float2* u1;
+  const float2* rhs_reg;   // nullable
+  float2* bout;            // recon: b = mu u + rhs_reg
+  int update_u;
+  float eps;
+  int maxit;
+  // bookkeeping
+  Loop L;
+  Partials P;
+  const float2* tw;        // [M] twiddles W_M^m (float)
+};
+
+// Generic column/row FFT passes (k_passes.cu): preconditioner, RSS init, encode/adjoint,
+// generic-mask matvec.
+struct PassArgs {
+  int B, C, M, N;
+  float mu, lam, gam;
+  const float2* tw_m;      // [M]
+  const float2* tw_n;      // [N]
+  const float* lam_inv;    // [B or 1][M][N] = 1/(N k)
+  int lam_bstride;         // M*N or 0
+  const uint8_t* mask;     // [B or 1][M][N]
+  int mask_bstride;
+  const float2* sens;      // [B][C][M][N]
+  // vectors
+  const float2* a0;
+  const float2* a1;
+  float2* o0;
+  float2* o1;
+  float2* tmp;             // [B][M][N] or [B][C][M][N]
+  float scale;
+  int mode;
+  int full;
+  Loop L;
+  Partials P;
+  // PCG p-update in the generic pass A
+  const float2* z;
+  float2* pbuf0;
+  float2* pbuf1;
+  float2* x;
+};
+
+// fp64 Lambda build (k_lambda.cu)
+struct LamArgs {
+  int B, C, M, N;
+  double mu, lam, gam;
+  const float2* sens;
+  const uint8_t* mask;
+  int mask_bstride;
+  int nmask;               // number of distinct masks (B or 1)
+  int nsens;               // number of distinct sens stacks (B)
+  double2* tmp;            // [B][C][M][N] fp64 scratch
+  double2* g;              // [B][M][N]
+  double2* rhat;           // [nmask][M][N]
+  double* k_out;           // [B][M][N]
+  float* lam_inv;          // [B][M][N]
+  const double2* tw_m;
+  const double2* tw_n;
+  int* bad;                // singular-k flag
+};
+
+struct SbArgs {
+  int B, M, N, levels;
+  float lam, gam;
+  const float2* x;
+  const float2* bx_in;
+  const float2* by_in;
+  float2* bx_out;
+  float2* by_out;
+  float2* bw;              // in place (block-local)
+  float2* rhs;             // rhs_reg out
+  const Scal* scal;        // nullable
+};
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_k1(int mode, bool separable, const K1Args& a, const CUtensorMap* tmap, int W, int G,
+                      cudaStream_t st);
+bool k1_supported(int M, int N);
+int k1_default_W(int M, int N);
+
+enum PassKind {
+  P_PRE_A_FWD_COL = 0,   // precond: r -= alpha q (PCG) ; col FFT fwd -> tmp
+  P_PRE_B_ROW = 1,       // precond: row FFT, x Lambda^-1, row IFFT (tmp in place)
+  P_PRE_C_INV_COL = 2,   // precond: col IFFT -> z ; <r, z>
+  P_ENC_COL = 3,         // encode: t_c = s_c x ; col FFT fwd -> tmp[b][c]
+  P_ENC_ROW = 4,         // encode: row FFT fwd, x mask / sqrt(N) -> y
+  P_ADJ_ROW = 5,         // adjoint/init: y masked, row IFFT -> tmp[b][c]
+  P_ADJ_COL = 6,         // adjoint/init: col IFFT, sum_c conj(s_c) . / sqrt(N) (+ RSS)
+  P_GEN_A_COL = 7,       // generic matvec: (p-update) ; t_c = s_c p ; col FFT fwd -> tmp[b][c]
+  P_GEN_B_ROW = 8,       // generic matvec: row FFT, x mask/N, row IFFT
+  P_NOPRE = 9,           // no preconditioner: r -= alpha q ; z = r ; partials
+  P_FIXUP = 10,          // x += alpha p (pending) / x = 0
+};
+cudaError_t launch_pass(int kind, const PassArgs& a, cudaStream_t st);
+bool pass_supported(int M, int N);
+
+cudaError_t launch_lambda_build(const LamArgs& a, cudaStream_t st);
+cudaError_t launch_sb_update(const SbArgs& a, cudaStream_t st);
+cudaError_t launch_log(const Loop& L, cudaStream_t st);
+
+}  // namespace sbk

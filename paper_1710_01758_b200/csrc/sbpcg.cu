@@ -1,0 +1,1018 @@
+// sbpcg.cu — libsbpcg host side: context, preconditioner build, device-driven PCG loop
+// (CUDA graph with a conditional WHILE node), Split Bregman orchestration, C ABI.
+//
+// Method: PAPER.md:87-244 (see include/sbpcg.h for per-call citations).  PyTorch is not
+// used here; the Python binding passes raw pointers and a cudaStream_t.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sbpcg.h"
+#include "kernels.cuh"
+
+using namespace sbk;
+
+struct GraphSlot {
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  int nfixed = 0;      // kernels outside the loop
+  int nbody = 0;       // kernels per loop iteration
+  float eps = -1.f;
+  int maxit = -1;
+  int precond = -1;
+};
+
+struct sb_ctx {
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  cudaStream_t cap2 = nullptr;  // body capture stream
+  int B = 0, C = 0, M = 0, N = 0, L = 0, mask_shared = 0;
+  float mu = 0, lam = 0, gam = 0;
+  bool separable = false;
+  int W = 8, G = 1;
+  size_t img = 0;
+  // constant data
+  float2* sens = nullptr;
+  uint8_t* mask = nullptr;
+  float* rowmask = nullptr;
+  float* lam_inv = nullptr;
+  double* kbuf = nullptr;
+  float2 *tw_m = nullptr, *tw_n = nullptr;
+  double2 *twd_m = nullptr, *twd_n = nullptr;
+  // vectors [B][M][N]
+  float2 *x = nullptr, *r = nullptr, *z = nullptr, *q = nullptr, *p0 = nullptr, *p1 = nullptr;
+  float2 *tmp = nullptr, *bvec = nullptr, *u = nullptr, *u1 = nullptr, *rhs = nullptr;
+  float2 *bx[2] = {nullptr, nullptr}, *by[2] = {nullptr, nullptr}, *bw = nullptr;
+  float2* tmpc = nullptr;  // [B][C][M][N]
+  float2* stage_in = nullptr;   // host staging [B][C][M][N]
+  float2* stage_out = nullptr;  // host staging [B][C][M][N]
+  // PCG bookkeeping
+  Scal* scal = nullptr;
+  Ctl* ctl = nullptr;
+  Partials P{};
+  float* hist = nullptr;
+  int hist_stride = 0;
+  int32_t* log_iters = nullptr;
+  float* log_relres = nullptr;
+  int log_cap = 0;
+  CUtensorMap tmap;
+  // graphs: 0 = solve, 1 = recon first, 2/3 = recon next (parity)
+  GraphSlot gs[4];
+  sb_status sticky = SB_OK;
+  std::string err;
+  int64_t launches = 0;
+  // kernel timing
+  bool timing = false;
+  double t_ms[2] = {0, 0};
+  int64_t t_n[2] = {0, 0};
+  std::vector<cudaEvent_t> evpool;
+  std::vector<std::pair<int, std::pair<int, int>>> evpend;  // (which, (ev0, ev1))
+  size_t evnext = 0;
+};
+
+// ------------------------------------------------------------------ error helpers
+static sb_status fail(sb_ctx* c, sb_status s, const std::string& msg) {
+  if (c) {
+    c->err = msg;
+    if (s == SB_E_CUDA) c->sticky = SB_E_CUDA;
+  }
+  return s;
+}
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(c, SB_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t n) {
+  return cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T));
+}
+
+static bool fft_len_ok(int64_t n) { return n == 8 || n == 16 || n == 32 || n == 64 || n == 128 || n == 256; }
+
+// ------------------------------------------------------------------ twiddles
+template <typename V>
+static std::vector<V> make_tw(int n) {
+  std::vector<V> t(n);
+  for (int m = 0; m < n; ++m) {
+    const double a = -2.0 * M_PI * (double)m / (double)n;
+    t[m].x = std::cos(a);
+    t[m].y = std::sin(a);
+  }
+  return t;
+}
+
+// ------------------------------------------------------------------ TMA descriptor
+static sb_status make_tmap(sb_ctx* c) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) return fail(c, SB_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  cuuint64_t gdim[3] = {(cuuint64_t)(2 * c->N), (cuuint64_t)c->M, (cuuint64_t)c->B * c->C};
+  cuuint64_t gstride[2] = {(cuuint64_t)c->N * 8, (cuuint64_t)c->M * c->N * 8};
+  cuuint32_t box[3] = {(cuuint32_t)(2 * c->W), (cuuint32_t)c->M, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&c->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)c->sens, gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(c, SB_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return SB_OK;
+}
+
+// ------------------------------------------------------------------ argument builders
+static Loop make_loop(sb_ctx* c, unsigned long long cond) {
+  Loop L;
+  L.scal = c->scal;
+  L.ctl = c->ctl;
+  L.hist = c->hist;
+  L.hist_stride = c->hist_stride;
+  L.log_iters = c->log_iters;
+  L.log_relres = c->log_relres;
+  L.B = c->B;
+  L.cond = cond;
+  return L;
+}
+
+static K1Args base_k1(sb_ctx* c) {
+  K1Args a;
+  memset(&a, 0, sizeof(a));
+  a.B = c->B;
+  a.C = c->C;
+  a.M = c->M;
+  a.N = c->N;
+  a.mu = c->mu;
+  a.lam = c->lam;
+  a.gam = c->gam;
+  a.rmask = c->rowmask;
+  a.rmask_bstride = c->mask_shared ? 0 : c->M;
+  a.tmpc = c->tmpc;
+  a.P = c->P;
+  a.tw = c->tw_m;
+  return a;
+}
+
+static PassArgs base_pass(sb_ctx* c) {
+  PassArgs a;
+  memset(&a, 0, sizeof(a));
+  a.B = c->B;
+  a.C = c->C;
+  a.M = c->M;
+  a.N = c->N;
+  a.mu = c->mu;
+  a.lam = c->lam;
+  a.gam = c->gam;
+  a.tw_m = c->tw_m;
+  a.tw_n = c->tw_n;
+  a.lam_inv = c->lam_inv;
+  a.lam_bstride = (int)c->img;
+  a.mask = c->mask;
+  a.mask_bstride = c->mask_shared ? 0 : (int)c->img;
+  a.sens = c->sens;
+  a.P = c->P;
+  a.pbuf0 = c->p0;
+  a.pbuf1 = c->p1;
+  a.x = c->x;
+  a.z = c->z;
+  return a;
+}
+
+// ------------------------------------------------------------------ timed launch wrappers
+static cudaEvent_t ev_get(sb_ctx* c) {
+  if (c->evnext >= c->evpool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->evpool.push_back(e);
+  }
+  return c->evpool[c->evnext++];
+}
+
+static sb_status run_k1(sb_ctx* c, int mode, const K1Args& a, cudaStream_t st) {
+  int e0 = -1;
+  if (c->timing) {
+    e0 = (int)c->evnext;
+    CK(cudaEventRecord(ev_get(c), st));
+  }
+  CK(launch_k1(mode, c->separable, a, &c->tmap, c->W, c->G, st));
+  if (c->timing) {
+    int e1 = (int)c->evnext;
+    CK(cudaEventRecord(ev_get(c), st));
+    c->evpend.push_back({0, {e0, e1}});
+  }
+  c->launches++;
+  return SB_OK;
+}
+
+static sb_status run_pass(sb_ctx* c, int kind, const PassArgs& a, cudaStream_t st) {
+  CK(launch_pass(kind, a, st));
+  c->launches++;
+  return SB_OK;
+}
+
+static void timing_collect(sb_ctx* c) {
+  for (auto& pe : c->evpend) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->evpool[pe.second.first], c->evpool[pe.second.second]) == cudaSuccess) {
+      c->t_ms[pe.first] += ms;
+      c->t_n[pe.first] += 1;
+    }
+  }
+  cudaGetLastError();
+  c->evpend.clear();
+  c->evnext = 0;
+}
+
+// ------------------------------------------------------------------ kernel sequences
+// q = A v (generic or separable)
+static sb_status seq_apply(sb_ctx* c, const float2* v, float2* out, cudaStream_t st) {
+  if (!c->separable) {
+    PassArgs pa = base_pass(c);
+    pa.a0 = v;
+    pa.tmp = c->tmpc;
+    pa.mode = 0;
+    pa.scale = 1.0f / (float)c->img;
+    sb_status s;
+    if ((s = run_pass(c, P_GEN_A_COL, pa, st))) return s;
+    if ((s = run_pass(c, P_GEN_B_ROW, pa, st))) return s;
+  }
+  K1Args a = base_k1(c);
+  a.vin = v;
+  a.out = out;
+  return run_k1(c, K1_APPLY, a, st);
+}
+
+// r0 = b - A x (+ recon RHS/feedback), fin_init
+static sb_status seq_resid(sb_ctx* c, Loop L, const float2* bgiven, bool recon, bool update_u, bool use_rhs,
+                           float eps, int maxit, cudaStream_t st) {
+  if (!c->separable) {
+    PassArgs pa = base_pass(c);
+    pa.a0 = c->x;
+    pa.tmp = c->tmpc;
+    pa.mode = 0;
+    pa.scale = 1.0f / (float)c->img;
+    sb_status s;
+    if ((s = run_pass(c, P_GEN_A_COL, pa, st))) return s;
+    if ((s = run_pass(c, P_GEN_B_ROW, pa, st))) return s;
+  }
+  K1Args a = base_k1(c);
+  a.vin = c->x;
+  a.out = c->r;
+  a.bvec = recon ? nullptr : bgiven;
+  a.u = c->u;
+  a.u1 = c->u1;
+  a.rhs_reg = use_rhs ? c->rhs : nullptr;
+  a.bout = c->bvec;
+  a.update_u = update_u ? 1 : 0;
+  a.eps = eps;
+  a.maxit = maxit;
+  a.L = L;
+  return run_k1(c, K1_RESID, a, st);
+}
+
+// z = M^{-1} r ; mode 0 = PCG init (rho_0), 1 = PCG iteration (r -= alpha q first),
+// -1 = standalone apply (no scalars)
+static sb_status seq_precond(sb_ctx* c, Loop L, int precond, int mode, const float2* rin, float2* zout,
+                             cudaStream_t st) {
+  PassArgs pa = base_pass(c);
+  pa.L = L;
+  pa.mode = mode;
+  sb_status s;
+  if (precond == 0) {
+    pa.a0 = c->r;
+    pa.a1 = c->q;
+    pa.o0 = c->r;
+    pa.o1 = c->z;
+    return run_pass(c, P_NOPRE, pa, st);
+  }
+  pa.a0 = rin;
+  pa.a1 = c->q;
+  pa.o0 = c->r;
+  pa.tmp = c->tmp;
+  if ((s = run_pass(c, P_PRE_A_FWD_COL, pa, st))) return s;
+  if ((s = run_pass(c, P_PRE_B_ROW, pa, st))) return s;
+  pa.a0 = (mode >= 0) ? c->r : nullptr;
+  pa.o0 = zout;
+  return run_pass(c, P_PRE_C_INV_COL, pa, st);
+}
+
+static sb_status seq_body(sb_ctx* c, Loop L, int precond, cudaStream_t st, int* nk) {
+  int n0 = (int)c->launches;
+  sb_status s;
+  if (!c->separable) {
+    PassArgs pa = base_pass(c);
+    pa.L = L;
+    pa.mode = 1;
+    pa.tmp = c->tmpc;
+    pa.scale = 1.0f / (float)c->img;
+    if ((s = run_pass(c, P_GEN_A_COL, pa, st))) return s;
+    if ((s = run_pass(c, P_GEN_B_ROW, pa, st))) return s;
+  }
+  K1Args a = base_k1(c);
+  a.z = c->z;
+  a.pbuf0 = c->p0;
+  a.pbuf1 = c->p1;
+  a.x = c->x;
+  a.out = c->q;
+  a.L = L;
+  if ((s = run_k1(c, K1_PCG, a, st))) return s;
+  if ((s = seq_precond(c, L, precond, 1, c->r, c->z, st))) return s;
+  if (nk) *nk = (int)c->launches - n0;
+  return SB_OK;
+}
+
+static sb_status seq_post(sb_ctx* c, Loop L, cudaStream_t st) {
+  PassArgs pa = base_pass(c);
+  pa.L = L;
+  sb_status s;
+  if ((s = run_pass(c, P_FIXUP, pa, st))) return s;
+  CK(launch_log(L, st));
+  c->launches++;
+  return SB_OK;
+}
+
+static sb_status seq_shrink(sb_ctx* c, int par, cudaStream_t st) {
+  SbArgs a;
+  memset(&a, 0, sizeof(a));
+  a.B = c->B;
+  a.M = c->M;
+  a.N = c->N;
+  a.levels = c->L;
+  a.lam = c->lam;
+  a.gam = c->gam;
+  a.x = c->x;
+  a.bx_in = c->bx[par];
+  a.by_in = c->by[par];
+  a.bx_out = c->bx[1 - par];
+  a.by_out = c->by[1 - par];
+  a.bw = c->bw;
+  a.rhs = c->rhs;
+  CK(launch_sb_update(a, st));
+  c->launches++;
+  return SB_OK;
+}
+
+static sb_status seq_init_recon(sb_ctx* c, const float2* ydev, cudaStream_t st) {
+  PassArgs pa = base_pass(c);
+  pa.a0 = ydev;
+  pa.tmp = c->tmpc;
+  pa.o0 = c->u1;
+  pa.o1 = c->x;
+  pa.scale = 1.0f / std::sqrt((float)c->img);
+  pa.full = 0;
+  sb_status s;
+  if ((s = run_pass(c, P_ADJ_ROW, pa, st))) return s;
+  if ((s = run_pass(c, P_ADJ_COL, pa, st))) return s;
+  CK(cudaMemcpyAsync(c->u, c->u1, c->img * c->B * sizeof(float2), cudaMemcpyDeviceToDevice, st));
+  return SB_OK;
+}
+
+// ------------------------------------------------------------------ graph building
+// kind: 0 solve (b in c->bvec), 1 recon first outer, 2/3 recon next outer (b-parity 0/1)
+static sb_status build_graph(sb_ctx* c, int kind, const sb_pcg_opts* o, const float2* ydev) {
+  GraphSlot& g = c->gs[kind];
+  if (g.exec && g.eps == o->eps && g.maxit == o->max_iters && g.precond == o->precond) return SB_OK;
+  if (g.exec) {
+    cudaGraphExecDestroy(g.exec);
+    cudaGraphDestroy(g.graph);
+    g.exec = nullptr;
+  }
+  cudaGraph_t G;
+  CK(cudaGraphCreate(&G, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, G, 0, 0));
+  Loop L = make_loop(c, (unsigned long long)h);
+  cudaStream_t cs = c->st;
+  int64_t l0 = c->launches;
+  bool saved_timing = c->timing;
+  c->timing = false;
+  CK(cudaStreamBeginCaptureToGraph(cs, G, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  sb_status s = SB_OK;
+  if (kind == 0) {
+    s = seq_resid(c, L, c->bvec, false, false, false, o->eps, o->max_iters, cs);
+  } else if (kind == 1) {
+    s = seq_init_recon(c, ydev, cs);
+    if (!s) s = seq_resid(c, L, nullptr, true, false, false, o->eps, o->max_iters, cs);
+  } else {
+    const int par = kind - 2;
+    s = seq_shrink(c, par, cs);
+    if (!s) s = seq_resid(c, L, nullptr, true, true, true, o->eps, o->max_iters, cs);
+  }
+  if (!s) s = seq_precond(c, L, o->precond, 0, c->r, c->z, cs);
+  if (s) {
+    cudaGraph_t dummy;
+    cudaStreamEndCapture(cs, &dummy);
+    c->timing = saved_timing;
+    return s;
+  }
+  cudaStreamCaptureStatus cst;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  CK(cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &deps, &ndeps));
+  alignas(cudaGraphNodeParams) unsigned char cpbuf[sizeof(cudaGraphNodeParams)];
+  memset(cpbuf, 0, sizeof(cpbuf));
+  cudaGraphNodeParams& cp = *reinterpret_cast<cudaGraphNodeParams*>(cpbuf);
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cnode;
+  CK(cudaGraphAddNode(&cnode, G, deps, ndeps, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CK(cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies));
+  const int64_t lb = c->launches;
+  CK(cudaStreamBeginCaptureToGraph(c->cap2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  int nk = 0;
+  s = seq_body(c, L, o->precond, c->cap2, &nk);
+  cudaGraph_t bodyout;
+  cudaError_t e2 = cudaStreamEndCapture(c->cap2, &bodyout);
+  if (s || e2 != cudaSuccess) {
+    cudaGraph_t dummy;
+    cudaStreamEndCapture(cs, &dummy);
+    c->timing = saved_timing;
+    if (s) return s;
+    CK(e2);
+  }
+  const int64_t la = c->launches;
+  s = seq_post(c, L, cs);
+  cudaGraph_t Gout;
+  cudaError_t e3 = cudaStreamEndCapture(cs, &Gout);
+  c->timing = saved_timing;
+  if (s) return s;
+  CK(e3);
+  CK(cudaGraphInstantiate(&g.exec, G, 0));
+  g.graph = G;
+  g.nbody = (int)(la - lb);
+  g.nfixed = (int)((lb - l0) + (c->launches - la));
+  c->launches = l0;  // capture does not launch
+  g.eps = o->eps;
+  g.maxit = o->max_iters;
+  g.precond = o->precond;
+  return SB_OK;
+}
+
+// eager (non-graph) execution of one solve whose prelude kind is given
+static sb_status eager_solve(sb_ctx* c, int kind, const sb_pcg_opts* o, const float2* ydev) {
+  Loop L = make_loop(c, 0ull);
+  sb_status s;
+  cudaStream_t st = c->st;
+  if (kind == 0) s = seq_resid(c, L, c->bvec, false, false, false, o->eps, o->max_iters, st);
+  else if (kind == 1) {
+    s = seq_init_recon(c, ydev, st);
+    if (!s) s = seq_resid(c, L, nullptr, true, false, false, o->eps, o->max_iters, st);
+  } else {
+    s = seq_shrink(c, kind - 2, st);
+    if (!s) s = seq_resid(c, L, nullptr, true, true, true, o->eps, o->max_iters, st);
+  }
+  if (s) return s;
+  if ((s = seq_precond(c, L, o->precond, 0, c->r, c->z, st))) return s;
+  int host_any = 1;
+  CK(cudaMemcpyAsync(&host_any, &c->ctl->any_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  while (host_any) {
+    if ((s = seq_body(c, L, o->precond, st, nullptr))) return s;
+    CK(cudaMemcpyAsync(&host_any, &c->ctl->any_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return seq_post(c, L, st);
+}
+
+static sb_status run_solve_kind(sb_ctx* c, int kind, const sb_pcg_opts* o, const float2* ydev) {
+  if (o->use_graph && !c->timing) {
+    sb_status s = build_graph(c, kind, o, ydev);
+    if (s) return s;
+    CK(cudaGraphLaunch(c->gs[kind].exec, c->st));
+    return SB_OK;
+  }
+  return eager_solve(c, kind, o, ydev);
+}
+
+// ------------------------------------------------------------------ Lambda build
+static sb_status build_lambda(sb_ctx* c) {
+  LamArgs a;
+  memset(&a, 0, sizeof(a));
+  a.B = c->B;
+  a.C = c->C;
+  a.M = c->M;
+  a.N = c->N;
+  a.mu = c->mu;
+  a.lam = c->lam;
+  a.gam = c->gam;
+  a.sens = c->sens;
+  a.mask = c->mask;
+  a.mask_bstride = c->mask_shared ? 0 : (int)c->img;
+  a.nmask = c->mask_shared ? 1 : c->B;
+  a.nsens = c->B;
+  a.k_out = c->kbuf;
+  a.lam_inv = c->lam_inv;
+  a.tw_m = c->twd_m;
+  a.tw_n = c->twd_n;
+  double2 *tmp = nullptr, *g = nullptr, *rh = nullptr;
+  int* bad = nullptr;
+  CK(dalloc(&tmp, (size_t)c->B * c->C * c->img));
+  CK(dalloc(&g, (size_t)c->B * c->img));
+  CK(dalloc(&rh, (size_t)a.nmask * c->img));
+  CK(dalloc(&bad, 1));
+  CK(cudaMemsetAsync(bad, 0, sizeof(int), c->st));
+  a.tmp = tmp;
+  a.g = g;
+  a.rhat = rh;
+  a.bad = bad;
+  CK(launch_lambda_build(a, c->st));
+  c->launches += 8;
+  int hb = 0;
+  CK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  cudaFree(tmp);
+  cudaFree(g);
+  cudaFree(rh);
+  cudaFree(bad);
+  if (hb) return fail(c, SB_E_SINGULAR_K, "singular k (min |k| <= 1e-14 or non-finite)");
+  return SB_OK;
+}
+
+// ------------------------------------------------------------------ staging helpers
+static sb_status stage_in(sb_ctx* c, const void* src, size_t bytes, const void** dev, void* scratch) {
+  if (is_device_ptr(src)) {
+    *dev = src;
+    return SB_OK;
+  }
+  CK(cudaMemcpyAsync(scratch, src, bytes, cudaMemcpyHostToDevice, c->st));
+  *dev = scratch;
+  return SB_OK;
+}
+
+static sb_status check_ready(sb_ctx* c) {
+  if (!c) return SB_E_ARG;
+  if (c->sticky) return c->sticky;
+  return SB_OK;
+}
+
+static sb_status status_from_scal(sb_ctx* c) {
+  std::vector<Scal> hs(c->B);
+  CK(cudaMemcpy(hs.data(), c->scal, sizeof(Scal) * c->B, cudaMemcpyDeviceToHost));
+  for (int b = 0; b < c->B; ++b) {
+    if (hs[b].status == ST_NONFINITE) return fail(c, SB_E_NONFINITE, "non-finite PCG scalar in problem " + std::to_string(b));
+    if (hs[b].status == ST_INDEFINITE) return fail(c, SB_E_INDEFINITE, "<p, A p> <= 0 in problem " + std::to_string(b));
+  }
+  return SB_OK;
+}
+
+// ================================================================== C ABI
+extern "C" {
+
+int32_t sb_abi_version(void) { return SBPCG_ABI_VERSION; }
+
+const char* sb_status_str(sb_status s) {
+  switch (s) {
+    case SB_OK: return "SB_OK";
+    case SB_E_ARG: return "SB_E_ARG";
+    case SB_E_DIM: return "SB_E_DIM";
+    case SB_E_UNSUPPORTED_SIZE: return "SB_E_UNSUPPORTED_SIZE";
+    case SB_E_PARAM: return "SB_E_PARAM";
+    case SB_E_SINGULAR_K: return "SB_E_SINGULAR_K";
+    case SB_E_NONFINITE: return "SB_E_NONFINITE";
+    case SB_E_INDEFINITE: return "SB_E_INDEFINITE";
+    case SB_E_CUDA: return "SB_E_CUDA";
+    case SB_E_NOMEM: return "SB_E_NOMEM";
+    case SB_E_COMM: return "SB_E_COMM";
+  }
+  return "SB_E_UNKNOWN";
+}
+
+const char* sb_last_error(const sb_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int64_t sb_kernel_launch_count(const sb_ctx* c) { return c ? c->launches : 0; }
+
+void sb_pcg_destroy(sb_ctx* c) {
+  if (!c) return;
+  cudaStreamSynchronize(c->st);
+  for (auto& g : c->gs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+  }
+  for (auto e : c->evpool) cudaEventDestroy(e);
+  void* bufs[] = {c->sens, c->mask, c->rowmask, c->lam_inv, c->kbuf, c->tw_m, c->tw_n, c->twd_m, c->twd_n,
+                  c->x, c->r, c->z, c->q, c->p0, c->p1, c->tmp, c->bvec, c->u, c->u1, c->rhs,
+                  c->bx[0], c->bx[1], c->by[0], c->by[1], c->bw, c->tmpc, c->stage_in, c->stage_out,
+                  c->scal, c->ctl, c->P.p0, c->P.p1, c->P.cnt, c->hist, c->log_iters, c->log_relres};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  if (c->cap2) cudaStreamDestroy(c->cap2);
+  delete c;
+}
+
+sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const uint8_t* mask, const sb_c64* sens,
+                        float mu, float lambda, float gamma, void* cuda_stream) {
+  if (!out) return SB_E_ARG;
+  *out = nullptr;
+  if (!dims || !mask || !sens) return SB_E_ARG;
+  if (dims->ndim != 2) return SB_E_DIM;
+  if (dims->batch < 1 || coils < 1 || dims->wavelet_levels < 0) return SB_E_DIM;
+  const int64_t M = dims->shape[0], N = dims->shape[1];
+  if (!fft_len_ok(M) || !fft_len_ok(N)) return SB_E_UNSUPPORTED_SIZE;
+  const int Lv = dims->wavelet_levels;
+  const int TH = M < 32 ? (int)M : 32, TW = N < 32 ? (int)N : 32;
+  if (Lv > 5 || (TH % (1 << Lv)) || (TW % (1 << Lv))) return SB_E_DIM;
+  if (!(gamma > 0.f) || mu < 0.f || lambda < 0.f || !std::isfinite(mu) || !std::isfinite(lambda) ||
+      !std::isfinite(gamma))
+    return SB_E_PARAM;
+
+  sb_ctx* c = new sb_ctx();
+  c->st = (cudaStream_t)cuda_stream;
+  cudaGetDevice(&c->dev);
+  c->B = dims->batch;
+  c->C = coils;
+  c->M = (int)M;
+  c->N = (int)N;
+  c->L = Lv;
+  c->mask_shared = dims->mask_shared ? 1 : 0;
+  c->mu = mu;
+  c->lam = lambda;
+  c->gam = gamma;
+  c->img = (size_t)M * N;
+  const size_t img = c->img, BN = (size_t)c->B * img, BCN = BN * c->C;
+  const size_t nmask = (c->mask_shared ? 1 : c->B) * img;
+
+  auto bail = [&](sb_status s) {
+    sb_pcg_destroy(c);
+    return s;
+  };
+  if (cudaStreamCreateWithFlags(&c->cap2, cudaStreamNonBlocking) != cudaSuccess) return bail(SB_E_CUDA);
+  bool ok = true;
+  ok &= dalloc(&c->sens, BCN) == cudaSuccess;
+  ok &= dalloc(&c->mask, nmask) == cudaSuccess;
+  ok &= dalloc(&c->rowmask, (size_t)(c->mask_shared ? 1 : c->B) * M) == cudaSuccess;
+  ok &= dalloc(&c->lam_inv, BN) == cudaSuccess;
+  ok &= dalloc(&c->kbuf, BN) == cudaSuccess;
+  ok &= dalloc(&c->tw_m, M) == cudaSuccess && dalloc(&c->tw_n, N) == cudaSuccess;
+  ok &= dalloc(&c->twd_m, M) == cudaSuccess && dalloc(&c->twd_n, N) == cudaSuccess;
+  float2** vecs[] = {&c->x, &c->r, &c->z, &c->q, &c->p0, &c->p1, &c->tmp, &c->bvec, &c->u, &c->u1, &c->rhs,
+                     &c->bx[0], &c->bx[1], &c->by[0], &c->by[1], &c->bw};
+  for (auto v : vecs) ok &= dalloc(v, BN) == cudaSuccess;
+  ok &= dalloc(&c->tmpc, BCN) == cudaSuccess;
+  ok &= dalloc(&c->scal, c->B) == cudaSuccess && dalloc(&c->ctl, 1) == cudaSuccess;
+  c->P.cap = 4096;
+  ok &= dalloc(&c->P.p0, (size_t)c->B * c->P.cap) == cudaSuccess;
+  ok &= dalloc(&c->P.p1, (size_t)c->B * c->P.cap) == cudaSuccess;
+  ok &= dalloc(&c->P.cnt, c->B) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    return bail(SB_E_NOMEM);
+  }
+  c->err.clear();
+  // copy inputs (host or device)
+  cudaMemcpyKind ks = is_device_ptr(sens) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  cudaMemcpyKind km = is_device_ptr(mask) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (cudaMemcpyAsync(c->sens, sens, BCN * sizeof(float2), ks, c->st) != cudaSuccess) return bail(SB_E_CUDA);
+  if (cudaMemcpyAsync(c->mask, mask, nmask, km, c->st) != cudaSuccess) return bail(SB_E_CUDA);
+  // separability (rows constant along d1) on the host
+  std::vector<uint8_t> hm(nmask);
+  if (cudaMemcpyAsync(hm.data(), c->mask, nmask, cudaMemcpyDeviceToHost, c->st) != cudaSuccess ||
+      cudaStreamSynchronize(c->st) != cudaSuccess)
+    return bail(SB_E_CUDA);
+  bool sep = true;
+  const int nm = c->mask_shared ? 1 : c->B;
+  std::vector<float> rm((size_t)nm * M);
+  for (int b = 0; b < nm && sep; ++b)
+    for (int64_t i = 0; i < M && sep; ++i) {
+      const uint8_t* row = hm.data() + (size_t)b * img + (size_t)i * N;
+      for (int64_t j = 0; j < N; ++j) {
+        if (row[j] > 1) {
+          sb_pcg_destroy(c);
+          return SB_E_ARG;
+        }
+        if (row[j] != row[0]) {
+          sep = false;
+          break;
+        }
+      }
+      rm[(size_t)b * M + i] = row[0] ? 1.0f / (float)M : 0.f;
+    }
+  c->separable = sep;
+  if (sep && cudaMemcpy(c->rowmask, rm.data(), rm.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
+    return bail(SB_E_CUDA);
+  // twiddles
+  auto tm = make_tw<float2>((int)M), tn = make_tw<float2>((int)N);
+  auto tdm = make_tw<double2>((int)M), tdn = make_tw<double2>((int)N);
+  if (cudaMemcpy(c->tw_m, tm.data(), M * sizeof(float2), cudaMemcpyHostToDevice) ||
+      cudaMemcpy(c->tw_n, tn.data(), N * sizeof(float2), cudaMemcpyHostToDevice) ||
+      cudaMemcpy(c->twd_m, tdm.data(), M * sizeof(double2), cudaMemcpyHostToDevice) ||
+      cudaMemcpy(c->twd_n, tdn.data(), N * sizeof(double2), cudaMemcpyHostToDevice))
+    return bail(SB_E_CUDA);
+  // zero state
+  for (auto v : vecs)
+    if (cudaMemsetAsync(*v, 0, BN * sizeof(float2), c->st) != cudaSuccess) return bail(SB_E_CUDA);
+  if (cudaMemsetAsync(c->P.cnt, 0, c->B * sizeof(unsigned int), c->st) ||
+      cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st) || cudaMemsetAsync(c->scal, 0, sizeof(Scal) * c->B, c->st))
+    return bail(SB_E_CUDA);
+  // K1 configuration: W columns per tile; G-CTA clusters split the coils when the
+  // problem alone would not fill the 148 SMs.
+  c->W = k1_default_W(c->M, c->N);
+  c->G = 1;
+  const int tiles = c->N / c->W;
+  for (int g = 2; g <= 8; g *= 2)
+    if (c->C % g == 0 && c->M % g == 0 && (int64_t)c->B * tiles * g <= 2 * 148) c->G = g;
+  sb_status s = make_tmap(c);
+  if (s) {
+    sb_pcg_destroy(c);
+    return s;
+  }
+  s = build_lambda(c);
+  if (s) {
+    sb_pcg_destroy(c);
+    return s;
+  }
+  *out = c;
+  return SB_OK;
+}
+
+sb_status sb_pcg_build_precond(sb_ctx* c) {
+  sb_status s = check_ready(c);
+  if (s) return s;
+  return build_lambda(c);
+}
+
+sb_status sb_pcg_apply_A(sb_ctx* c, const sb_c64* x, sb_c64* y) {
+  sb_status s = check_ready(c);
+  if (s) return s;
+  if (!x || !y || (const void*)x == (const void*)y) return fail(c, SB_E_ARG, "apply_A: bad pointers");
+  const size_t bytes = c->B * c->img * sizeof(float2);
+  const bool hy = !is_device_ptr(y);
+  const void* xd;
+  if ((s = stage_in(c, x, bytes, &xd, c->tmp))) return s;
+  float2* yd = hy ? c->q : (float2*)y;
+  if ((s = seq_apply(c, (const float2*)xd, yd, c->st))) return s;
+  if (hy) {
+    CK(cudaMemcpyAsync(y, yd, bytes, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  }
+  return SB_OK;
+}
+
+sb_status sb_pcg_apply_Pinv(sb_ctx* c, const sb_c64* r, sb_c64* z) {
+  sb_status s = check_ready(c);
+  if (s) return s;
+  if (!r || !z || (const void*)r == (const void*)z) return fail(c, SB_E_ARG, "apply_Pinv: bad pointers");
+  const size_t bytes = c->B * c->img * sizeof(float2);
+  const bool hz = !is_device_ptr(z);
+  const void* rd;
+  if ((s = stage_in(c, r, bytes, &rd, c->q))) return s;
+  float2* zd = hz ? c->z : (float2*)z;
+  Loop L = make_loop(c, 0ull);
+  L.scal = nullptr;
+  if ((s = seq_precond(c, L, 1, -1, (const float2*)rd, zd, c->st))) return s;
+  if (hz) {
+    CK(cudaMemcpyAsync(z, zd, bytes, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  }
+  return SB_OK;
+}
+
+sb_status sb_encode(sb_ctx* c, const sb_c64* x, sb_c64* y, int32_t full) {
+  sb_status s = check_ready(c);
+  if (s) return s;
+  if (!x || !y || (const void*)x == (const void*)y) return fail(c, SB_E_ARG, "encode: bad pointers");
+  const size_t bytes = c->B * c->img * sizeof(float2), ybytes = bytes * c->C;
+  const bool hy = !is_device_ptr(y);
+  const void* xd;
+  if ((s = stage_in(c, x, bytes, &xd, c->tmp))) return s;
+  if (hy && !c->stage_out) CK(dalloc(&c->stage_out, c->B * c->C * c->img));
+  float2* yd = hy ? c->stage_out : (float2*)y;
+  PassArgs pa = base_pass(c);
+  pa.a0 = (const float2*)xd;
+  pa.tmp = c->tmpc;
+  pa.o0 = yd;
+  pa.full = full ? 1 : 0;
+  pa.scale = 1.0f / std::sqrt((float)c->img);
+  if ((s = run_pass(c, P_ENC_COL, pa, c->st))) return s;
+  if ((s = run_pass(c, P_ENC_ROW, pa, c->st))) return s;
+  if (hy) {
+    CK(cudaMemcpyAsync(y, yd, ybytes, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  }
+  return SB_OK;
+}
+
+sb_status sb_adjoint(sb_ctx* c, const sb_c64* y, sb_c64* x) {
+  sb_status s = check_ready(c);
+  if (s) return s;
+  if (!x || !y || (const void*)x == (const void*)y) return fail(c, SB_E_ARG, "adjoint: bad pointers");
+  const size_t bytes = c->B * c->img * sizeof(float2), ybytes = bytes * c->C;
+  const bool hx = !is_device_ptr(x);
+  if (!is_device_ptr(y) && !c->stage_in) CK(dalloc(&c->stage_in, c->B * c->C * c->img));
+  const void* yd;
+  if ((s = stage_in(c, y, ybytes, &yd, c->stage_in))) return s;
+  float2* xd = hx ? c->q : (float2*)x;
+  PassArgs pa = base_pass(c);
+  pa.a0 = (const float2*)yd;
+  pa.tmp = c->tmpc;
+  pa.o0 = xd;
+  pa.o1 = nullptr;
+  pa.scale = 1.0f / std::sqrt((float)c->img);
+  if ((s = run_pass(c, P_ADJ_ROW, pa, c->st))) return s;
+  if ((s = run_pass(c, P_ADJ_COL, pa, c->st))) return s;
+  if (hx) {
+    CK(cudaMemcpyAsync(x, xd, bytes, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  }
+  return SB_OK;
+}
+
+static sb_status check_opts(sb_ctx* c, const sb_pcg_opts* o) {
+  if (!o || o->max_iters < 1 || !(o->eps >= 0.f) || (o->precond != 0 && o->precond != 1))
+    return fail(c, SB_E_ARG, "bad pcg options");
+  return SB_OK;
+}
+
+static sb_status ensure_hist(sb_ctx* c, int maxit, int slots) {
+  if (c->hist_stride < maxit + 1) {
+    if (c->hist) cudaFree(c->hist);
+    c->hist = nullptr;
+    CK(dalloc(&c->hist, (size_t)c->B * (maxit + 1)));
+    c->hist_stride = maxit + 1;
+    for (auto& g : c->gs) g.maxit = -1;  // graphs captured the old pointer
+  }
+  if (c->log_cap < slots) {
+    if (c->log_iters) cudaFree(c->log_iters);
+    if (c->log_relres) cudaFree(c->log_relres);
+    CK(dalloc(&c->log_iters, (size_t)c->B * slots));
+    CK(dalloc(&c->log_relres, (size_t)c->B * slots));
+    c->log_cap = slots;
+    for (auto& g : c->gs) g.maxit = -1;
+  }
+  return SB_OK;
+}
+
+sb_status sb_pcg_solve(sb_ctx* c, const sb_c64* b, sb_c64* x, const sb_pcg_opts* o, sb_pcg_stats* stats) {
+  sb_status s = check_ready(c);
+  if (s) return s;
+  if (!b || !x || (const void*)b == (const void*)x) return fail(c, SB_E_ARG, "solve: bad pointers");
+  if ((s = check_opts(c, o))) return s;
+  if ((s = ensure_hist(c, o->max_iters, 1))) return s;
+  const size_t bytes = c->B * c->img * sizeof(float2);
+  const cudaMemcpyKind kb = is_device_ptr(b) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  const bool xdev = is_device_ptr(x);
+  CK(cudaMemcpyAsync(c->bvec, b, bytes, kb, c->st));
+  CK(cudaMemcpyAsync(c->x, x, bytes, xdev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st));
+  if (c->timing) c->evnext = 0;
+  if ((s = run_solve_kind(c, 0, o, nullptr))) return s;
+  CK(cudaMemcpyAsync(x, c->x, bytes, xdev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (c->timing) timing_collect(c);
+  std::vector<Scal> hs(c->B);
+  CK(cudaMemcpy(hs.data(), c->scal, sizeof(Scal) * c->B, cudaMemcpyDeviceToHost));
+  if (o->use_graph && !c->timing) {
+    int mx = 0;
+    for (auto& h : hs) mx = std::max(mx, h.iter);
+    c->launches += c->gs[0].nfixed + (int64_t)c->gs[0].nbody * mx;
+  }
+  if (stats) {
+    std::vector<float> hist;
+    if (stats->relres_hist) {
+      hist.resize((size_t)c->B * c->hist_stride);
+      CK(cudaMemcpy(hist.data(), c->hist, hist.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    }
+    for (int i = 0; i < c->B; ++i) {
+      if (stats->iters) stats->iters[i] = hs[i].iter;
+      if (stats->converged) stats->converged[i] = (int8_t)hs[i].converged;
+      if (stats->final_relres) stats->final_relres[i] = hs[i].nb2 > 0 ? (float)std::sqrt(hs[i].rr / hs[i].nb2) : 0.f;
+      if (stats->relres_hist)
+        for (int k = 0; k <= o->max_iters; ++k)
+          stats->relres_hist[(size_t)i * (o->max_iters + 1) + k] = hist[(size_t)i * c->hist_stride + k];
+    }
+  }
+  return status_from_scal(c);
+}
+
+sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* x_out, sb_recon_log* log) {
+  sb_status s = check_ready(c);
+  if (s) return s;
+  if (!y || !x_out || !ro || (const void*)y == (const void*)x_out) return fail(c, SB_E_ARG, "recon: bad pointers");
+  if (ro->n_outer < 1 || ro->n_inner != 1) return fail(c, SB_E_ARG, "recon: n_outer >= 1 and n_inner == 1 required");
+  if ((s = check_opts(c, &ro->pcg))) return s;
+  if ((s = ensure_hist(c, ro->pcg.max_iters, ro->n_outer))) return s;
+  const size_t bytes = c->B * c->img * sizeof(float2), ybytes = bytes * c->C;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, c->st));
+  // y is always copied into the context's staging buffer so the cached graphs stay valid
+  if (!c->stage_in) CK(dalloc(&c->stage_in, c->B * c->C * c->img));
+  CK(cudaMemcpyAsync(c->stage_in, y, ybytes, is_device_ptr(y) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     c->st));
+  const void* yd = c->stage_in;
+  // fresh SB state (Alg. 1 step 1)
+  float2* zs[] = {c->bx[0], c->bx[1], c->by[0], c->by[1], c->bw, c->rhs};
+  for (auto v : zs) CK(cudaMemsetAsync(v, 0, bytes, c->st));
+  CK(cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st));
+  if (c->timing) c->evnext = 0;
+  const sb_pcg_opts* o = &ro->pcg;
+  if ((s = run_solve_kind(c, 1, o, (const float2*)yd))) return s;
+  for (int j = 1; j < ro->n_outer; ++j) {
+    const int par = (j - 1) & 1;  // b_x/b_y buffer parity
+    if ((s = run_solve_kind(c, 2 + par, o, nullptr))) return s;
+  }
+  // final shrink/Bregman step of the last inner iteration (Alg. 1 steps 6-11); the final
+  // data feedback (steps 13-15) does not change x and is skipped.
+  if ((s = seq_shrink(c, (ro->n_outer - 1) & 1, c->st))) return s;
+  CK(cudaMemcpyAsync(x_out, c->x, bytes, is_device_ptr(x_out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaEventRecord(e1, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (c->timing) timing_collect(c);
+  std::vector<int32_t> li((size_t)ro->n_outer * c->B);
+  std::vector<float> lr((size_t)ro->n_outer * c->B);
+  CK(cudaMemcpy(li.data(), c->log_iters, li.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(lr.data(), c->log_relres, lr.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  if (o->use_graph && !c->timing) {
+    for (int j = 0; j < ro->n_outer; ++j) {
+      int mx = 0;
+      for (int b = 0; b < c->B; ++b) mx = std::max(mx, li[(size_t)j * c->B + b]);
+      const GraphSlot& g = c->gs[j == 0 ? 1 : 2 + ((j - 1) & 1)];
+      c->launches += g.nfixed + (int64_t)g.nbody * mx;
+    }
+  }
+  if (log) {
+    if (log->pcg_iters) memcpy(log->pcg_iters, li.data(), li.size() * sizeof(int32_t));
+    if (log->final_relres) memcpy(log->final_relres, lr.data(), lr.size() * sizeof(float));
+    log->total_ms = ms;
+  }
+  return status_from_scal(c);
+}
+
+sb_status sb_sb_update(sb_ctx* c, const sb_c64* x, sb_c64* bx, sb_c64* by, sb_c64* bw, sb_c64* rhs_reg) {
+  sb_status s = check_ready(c);
+  if (s) return s;
+  if (!x || !bx || !by || !bw || !rhs_reg) return fail(c, SB_E_ARG, "sb_update: null pointer");
+  const size_t bytes = c->B * c->img * sizeof(float2);
+  auto kin = [&](const void* p) { return is_device_ptr(p) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice; };
+  auto kout = [&](const void* p) { return is_device_ptr(p) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost; };
+  CK(cudaMemcpyAsync(c->x, x, bytes, kin(x), c->st));
+  CK(cudaMemcpyAsync(c->bx[0], bx, bytes, kin(bx), c->st));
+  CK(cudaMemcpyAsync(c->by[0], by, bytes, kin(by), c->st));
+  CK(cudaMemcpyAsync(c->bw, bw, bytes, kin(bw), c->st));
+  if ((s = seq_shrink(c, 0, c->st))) return s;
+  CK(cudaMemcpyAsync(bx, c->bx[1], bytes, kout(bx), c->st));
+  CK(cudaMemcpyAsync(by, c->by[1], bytes, kout(by), c->st));
+  CK(cudaMemcpyAsync(bw, c->bw, bytes, kout(bw), c->st));
+  CK(cudaMemcpyAsync(rhs_reg, c->rhs, bytes, kout(rhs_reg), c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return SB_OK;
+}
+
+sb_status sb_pcg_get_k(sb_ctx* c, double* k_out) {
+  sb_status s = check_ready(c);
+  if (s) return s;
+  if (!k_out) return fail(c, SB_E_ARG, "get_k: null");
+  const size_t bytes = c->B * c->img * sizeof(double);
+  CK(cudaMemcpyAsync(k_out, c->kbuf, bytes, is_device_ptr(k_out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return SB_OK;
+}
+
+sb_status sb_set_kernel_timing(sb_ctx* c, int32_t enable) {
+  if (!c) return SB_E_ARG;
+  c->timing = enable != 0;
+  c->t_ms[0] = c->t_ms[1] = 0;
+  c->t_n[0] = c->t_n[1] = 0;
+  return SB_OK;
+}
+
+sb_status sb_get_kernel_time(sb_ctx* c, int32_t which, double* ms, int64_t* launches, double* alg_bytes) {
+  if (!c || which < 0 || which > 1) return SB_E_ARG;
+  if (ms) *ms = c->t_ms[which];
+  if (launches) *launches = c->t_n[which];
+  if (alg_bytes) {
+    // K1 (PCG mode) algorithmic bytes per launch, per problem:
+    // coil maps 8NC + z, p_old, x read + x, p_new, q written (6 x 8N) + mask (4M)
+    const double N = (double)c->img;
+    *alg_bytes = which == 0 ? (double)c->B * (8.0 * N * c->C + 6.0 * 8.0 * N + 4.0 * c->M)
+                            : (double)c->B * (4.0 * 8.0 * N + 4.0 * N);
+  }
+  return SB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,221 @@
+"""Thin ctypes binding of libsbpcg (include/sbpcg.h): argument marshalling only.
+
+Every step of the method runs in the CUDA library; there is no CPU fallback: if the
+shared library is missing or fails to load, importing this module raises.  Tensors are
+torch tensors (device memory, streams); the library receives raw pointers.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsbpcg.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libsbpcg.so not built ({LIB_PATH}); run `python -m paper_1710_01758_b200.build`")
+_lib = C.CDLL(LIB_PATH)
+
+
+class SbDims(C.Structure):
+    _fields_ = [("ndim", C.c_int32), ("shape", C.c_int64 * 3), ("batch", C.c_int32),
+                ("wavelet_levels", C.c_int32), ("mask_shared", C.c_int32)]
+
+
+class SbPcgOpts(C.Structure):
+    _fields_ = [("eps", C.c_float), ("max_iters", C.c_int32), ("precond", C.c_int32),
+                ("use_graph", C.c_int32)]
+
+
+class SbPcgStats(C.Structure):
+    _fields_ = [("iters", C.POINTER(C.c_int32)), ("final_relres", C.POINTER(C.c_float)),
+                ("converged", C.POINTER(C.c_int8)), ("relres_hist", C.POINTER(C.c_float))]
+
+
+class SbReconOpts(C.Structure):
+    _fields_ = [("n_outer", C.c_int32), ("n_inner", C.c_int32), ("pcg", SbPcgOpts)]
+
+
+class SbReconLog(C.Structure):
+    _fields_ = [("pcg_iters", C.POINTER(C.c_int32)), ("final_relres", C.POINTER(C.c_float)),
+                ("total_ms", C.c_double)]
+
+
+_vp = C.c_void_p
+_sig = {
+    "sb_pcg_create": (C.c_int, [C.POINTER(_vp), C.POINTER(SbDims), C.c_int32, _vp, _vp, C.c_float,
+                                C.c_float, C.c_float, _vp]),
+    "sb_pcg_build_precond": (C.c_int, [_vp]),
+    "sb_pcg_apply_A": (C.c_int, [_vp, _vp, _vp]),
+    "sb_pcg_apply_Pinv": (C.c_int, [_vp, _vp, _vp]),
+    "sb_encode": (C.c_int, [_vp, _vp, _vp, C.c_int32]),
+    "sb_adjoint": (C.c_int, [_vp, _vp, _vp]),
+    "sb_pcg_solve": (C.c_int, [_vp, _vp, _vp, C.POINTER(SbPcgOpts), C.POINTER(SbPcgStats)]),
+    "sb_recon": (C.c_int, [_vp, _vp, C.POINTER(SbReconOpts), _vp, C.POINTER(SbReconLog)]),
+    "sb_sb_update": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "sb_pcg_get_k": (C.c_int, [_vp, _vp]),
+    "sb_set_kernel_timing": (C.c_int, [_vp, C.c_int32]),
+    "sb_get_kernel_time": (C.c_int, [_vp, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_double)]),
+    "sb_kernel_launch_count": (C.c_int64, [_vp]),
+    "sb_pcg_destroy": (None, [_vp]),
+    "sb_status_str": (C.c_char_p, [C.c_int]),
+    "sb_last_error": (C.c_char_p, [_vp]),
+    "sb_abi_version": (C.c_int32, []),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_sig)
+
+STATUS = {0: "SB_OK", 1: "SB_E_ARG", 2: "SB_E_DIM", 3: "SB_E_UNSUPPORTED_SIZE", 4: "SB_E_PARAM",
+          5: "SB_E_SINGULAR_K", 6: "SB_E_NONFINITE", 7: "SB_E_INDEFINITE", 8: "SB_E_CUDA",
+          9: "SB_E_NOMEM", 10: "SB_E_COMM"}
+
+
+class SbError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _ptr(t: torch.Tensor) -> int:
+    if not t.is_contiguous():
+        raise ValueError("tensors must be C-contiguous")
+    return t.data_ptr()
+
+
+class SbPcg:
+    """Context for A = mu sum_c (RFS_c)^H RFS_c + lam sum_d D_d^H D_d + gamma W^H W and the
+    circulant preconditioner M^{-1} = F^H diag{k}^{-1} F."""
+
+    def __init__(self, sens: torch.Tensor, mask: torch.Tensor, mu: float, lam: float, gamma: float,
+                 levels: int = 1, stream: Optional[torch.cuda.Stream] = None):
+        if sens.dim() == 3:
+            sens = sens.unsqueeze(0)
+        if sens.dtype != torch.complex64 or mask.dtype != torch.uint8:
+            raise TypeError("sens must be complex64 [B,C,M,N], mask uint8 [B,M,N] or [M,N]")
+        B, Cc, M, N = sens.shape
+        shared = mask.dim() == 2 or (mask.dim() == 3 and mask.shape[0] == 1 and B > 1)
+        self.B, self.C, self.M, self.N = B, Cc, M, N
+        self.device = sens.device if sens.is_cuda else torch.device("cuda", torch.cuda.current_device())
+        self._stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self._sens = sens.contiguous()
+        self._mask = mask.contiguous()
+        d = SbDims(2, (C.c_int64 * 3)(M, N, 0), B, levels, 1 if shared else 0)
+        h = _vp()
+        st = _lib.sb_pcg_create(C.byref(h), C.byref(d), Cc, _ptr(self._mask), _ptr(self._sens),
+                                float(mu), float(lam), float(gamma), _vp(self._stream.cuda_stream))
+        if st != 0:
+            raise SbError(st, "sb_pcg_create failed")
+        self._h = h
+        self.mu, self.lam, self.gamma, self.levels = mu, lam, gamma, levels
+
+    # ------------------------------------------------------------------
+    def _check(self, st: int, what: str):
+        if st != 0:
+            raise SbError(st, f"{what}: {_lib.sb_last_error(self._h).decode()}")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.sb_pcg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _img(self, like: Optional[torch.Tensor] = None, coils: bool = False, device=None):
+        shape = (self.B, self.C, self.M, self.N) if coils else (self.B, self.M, self.N)
+        dev = device if device is not None else (like.device if like is not None else self.device)
+        return torch.empty(shape, dtype=torch.complex64, device=dev,
+                           pin_memory=(dev.type == "cpu" and torch.cuda.is_available()))
+
+    # ------------------------------------------------------------------ operators
+    def build_precond(self):
+        self._check(_lib.sb_pcg_build_precond(self._h), "build_precond")
+
+    def apply_A(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        y = out if out is not None else self._img(x)
+        self._check(_lib.sb_pcg_apply_A(self._h, _ptr(x), _ptr(y)), "apply_A")
+        return y
+
+    def apply_Pinv(self, r: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        z = out if out is not None else self._img(r)
+        self._check(_lib.sb_pcg_apply_Pinv(self._h, _ptr(r), _ptr(z)), "apply_Pinv")
+        return z
+
+    def encode(self, x: torch.Tensor, full: bool = False, out: Optional[torch.Tensor] = None):
+        y = out if out is not None else self._img(x, coils=True)
+        self._check(_lib.sb_encode(self._h, _ptr(x), _ptr(y), 1 if full else 0), "encode")
+        return y
+
+    def adjoint(self, y: torch.Tensor, out: Optional[torch.Tensor] = None):
+        x = out if out is not None else self._img(y)
+        self._check(_lib.sb_adjoint(self._h, _ptr(y), _ptr(x)), "adjoint")
+        return x
+
+    def get_k(self) -> torch.Tensor:
+        k = torch.empty((self.B, self.M, self.N), dtype=torch.float64)
+        self._check(_lib.sb_pcg_get_k(self._h, _ptr(k)), "get_k")
+        return k
+
+    def solve(self, b: torch.Tensor, x0: torch.Tensor, eps: float = 1e-4, max_iters: int = 50,
+              precond: int = 1, use_graph: bool = True, history: bool = False):
+        x = x0.clone()
+        iters = (C.c_int32 * self.B)()
+        rel = (C.c_float * self.B)()
+        conv = (C.c_int8 * self.B)()
+        hist = (C.c_float * (self.B * (max_iters + 1)))() if history else None
+        st = SbPcgStats(iters, rel, conv, hist)
+        o = SbPcgOpts(float(eps), int(max_iters), int(precond), 1 if use_graph else 0)
+        self._check(_lib.sb_pcg_solve(self._h, _ptr(b), _ptr(x), C.byref(o), C.byref(st)), "solve")
+        out = dict(iters=list(iters), final_relres=list(rel), converged=[bool(v) for v in conv])
+        if history:
+            out["relres_hist"] = [list(hist[i * (max_iters + 1):(i + 1) * (max_iters + 1)])
+                                  for i in range(self.B)]
+        return x, out
+
+    def recon(self, y: torch.Tensor, n_outer: int, eps: float = 1e-4, max_iters: int = 50,
+              precond: int = 1, use_graph: bool = True, out: Optional[torch.Tensor] = None):
+        x = out if out is not None else self._img(y)
+        it = (C.c_int32 * (n_outer * self.B))()
+        rel = (C.c_float * (n_outer * self.B))()
+        log = SbReconLog(it, rel, 0.0)
+        o = SbReconOpts(int(n_outer), 1, SbPcgOpts(float(eps), int(max_iters), int(precond),
+                                                   1 if use_graph else 0))
+        self._check(_lib.sb_recon(self._h, _ptr(y), C.byref(o), _ptr(x), C.byref(log)), "recon")
+        iters = [[it[j * self.B + b] for b in range(self.B)] for j in range(n_outer)]
+        rels = [[rel[j * self.B + b] for b in range(self.B)] for j in range(n_outer)]
+        return x, dict(pcg_iters=iters, final_relres=rels, total_ms=log.total_ms)
+
+    def sb_update(self, x, bx, by, bw):
+        bx, by, bw = bx.clone(), by.clone(), bw.clone()
+        rhs = torch.empty_like(x)
+        self._check(_lib.sb_sb_update(self._h, _ptr(x), _ptr(bx), _ptr(by), _ptr(bw), _ptr(rhs)),
+                    "sb_update")
+        return bx, by, bw, rhs
+
+    # ------------------------------------------------------------------ instrumentation
+    def set_kernel_timing(self, on: bool):
+        self._check(_lib.sb_set_kernel_timing(self._h, 1 if on else 0), "set_kernel_timing")
+
+    def kernel_time(self, which: int = 0):
+        ms, n, by = C.c_double(), C.c_int64(), C.c_double()
+        self._check(_lib.sb_get_kernel_time(self._h, which, C.byref(ms), C.byref(n), C.byref(by)),
+                    "kernel_time")
+        return ms.value, n.value, by.value
+
+    def launches(self) -> int:
+        return int(_lib.sb_kernel_launch_count(self._h))
+
+
+def abi_version() -> int:
+    return int(_lib.sb_abi_version())
