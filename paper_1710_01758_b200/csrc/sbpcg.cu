@@ -30,6 +30,7 @@ struct GraphSlot {
 struct sb_ctx {
   int dev = 0;
   cudaStream_t st = nullptr;
+  cudaStream_t cap1 = nullptr;  // graph capture stream (the user stream may be the legacy NULL stream)
   cudaStream_t cap2 = nullptr;  // body capture stream
   int B = 0, C = 0, M = 0, N = 0, L = 0, mask_shared = 0;
   float mu = 0, lam = 0, gam = 0;
@@ -398,7 +399,7 @@ static sb_status build_graph(sb_ctx* c, int kind, const sb_pcg_opts* o, const fl
   cudaGraphConditionalHandle h;
   CK(cudaGraphConditionalHandleCreate(&h, G, 0, 0));
   Loop L = make_loop(c, (unsigned long long)h);
-  cudaStream_t cs = c->st;
+  cudaStream_t cs = c->cap1;
   int64_t l0 = c->launches;
   bool saved_timing = c->timing;
   c->timing = false;
@@ -614,6 +615,7 @@ void sb_pcg_destroy(sb_ctx* c) {
                   c->scal, c->ctl, c->P.p0, c->P.p1, c->P.cnt, c->hist, c->log_iters, c->log_relres};
   for (void* p : bufs)
     if (p) cudaFree(p);
+  if (c->cap1) cudaStreamDestroy(c->cap1);
   if (c->cap2) cudaStreamDestroy(c->cap2);
   delete c;
 }
@@ -654,7 +656,9 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
     sb_pcg_destroy(c);
     return s;
   };
-  if (cudaStreamCreateWithFlags(&c->cap2, cudaStreamNonBlocking) != cudaSuccess) return bail(SB_E_CUDA);
+  if (cudaStreamCreateWithFlags(&c->cap1, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->cap2, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(SB_E_CUDA);
   bool ok = true;
   ok &= dalloc(&c->sens, BCN) == cudaSuccess;
   ok &= dalloc(&c->mask, nmask) == cudaSuccess;
