@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""bench.py — PCG iterations/s and SB reconstruction time on B200 (BASELINE.json metric).
+
+One STEP = one pass of the whole hot path on one batch of synthetic input:
+  Lambda build + Split Bregman reconstruction (a1-a13): 20 outer
+  iterations, each a device-driven PCG solve (tol 1e-4, max 50) with the circulant
+  preconditioner, shrink/Bregman updates and data feedback.
+Default workload: BASELINE.json configs[1] ("config 2"): 256x256, 12 coils, VD line mask
+R=4 with a 24-line centre, TV + 3-level Haar, mu=1, lambda=gamma=0.02.  Inputs are seeded
+synthetic phantoms/coil maps/masks (synth/), k-space formed on the GPU with the library's
+own encoder (sb_encode).  With --gpus N (torchrun), each rank reconstructs its own
+independent slice (weak scaling, no data-path collective).
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle instead
+(bounded sample per step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = synth_metric = ("PCG iters/s & SB recon time (256²×12-coil); "
+                         "HBM GB/s as fraction of B200 peak")
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precond", type=int, default=1)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slices", type=int, default=0, help="override problems per rank")
+    return ap.parse_args()
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload(cfg: int, ws: int, rank: int, slices_override: int):
+    spec = synth.CONFIGS[cfg]
+    if cfg == 3:
+        per = slices_override or max(1, spec.batch // ws)
+        first = rank * per
+    else:
+        per = slices_override or 1
+        first = rank * per
+    return spec, per, first
+
+
+def make_inputs(cfg, first, per):
+    ps = [synth.problem2d(cfg, s) for s in range(first, first + per)]
+    phantom = np.stack([p["phantom"] for p in ps])
+    sens = np.stack([p["sens"] for p in ps])
+    mask = np.stack([p["mask"] for p in ps])
+    noise = np.stack([p["noise"] for p in ps])
+    return phantom, sens, mask, noise
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out, _ = self.p.communicate()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def load_traffic(cfg):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d.get(f"config{cfg}")
+    return None
+
+
+# ---------------------------------------------------------------------------------------
+def run_reference(args):
+    """CPU oracle arm (oracle/ as it stands), bounded sample per step: one SB outer iteration
+    (Alg. 1 steps 4-15, literal per-coil k-space feedback) of the same workload."""
+    ws, rank, _ = dist_setup()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        if rank != 0:
+            dist.barrier()
+            return
+    from oracle import problems, sb
+    spec, per, first = workload(args.config, 1, 0, args.slices)
+    p = synth.problem2d(args.config, first)
+    y = problems.make_kspace(p["phantom"], p["sens"], p["mask"], p["noise"])
+    prm = spec.params
+
+    def sample():
+        t = time.perf_counter()
+        x, log = sb.sb_recon(y, p["sens"], p["mask"], prm.mu, prm.lam, prm.gamma, 1, 1,
+                             prm.wavelet_levels, prm.eps, prm.max_iters,
+                             "circulant" if args.precond else "none")
+        return time.perf_counter() - t, sum(log.pcg_iters)
+
+    for _ in range(args.warmup):
+        sample()
+    tot_t, tot_it = 0.0, 0
+    for _ in range(args.steps):
+        dt, it = sample()
+        tot_t += dt
+        tot_it += it
+    value = tot_it / tot_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "PCG iters/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded phantom/coils/mask)",
+        "config": {"workload": spec.name, "sample": "1 SB outer iteration per step (oracle)",
+                   "mask": "VD lines" if spec.mask_kind == "lines" else "random2d"},
+        "cpu_baseline": {"value": value, "unit": "PCG iters/s", "cores": 1, "kind": "oracle",
+                         "sample": "1 SB outer iteration of slice 0 per step"},
+        "e2e": {"value": value, "unit": "PCG iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_baseline_sample(cfg, precond):
+    """Oracle PCG iterations/s on a bounded sample: the first 2 SB outer iterations of slice 0
+    (about 10-30 s of single-threaded numpy work at config 2)."""
+    from oracle import problems, sb
+    spec = synth.CONFIGS[cfg]
+    p = synth.problem2d(cfg, 0)
+    y = problems.make_kspace(p["phantom"], p["sens"], p["mask"], p["noise"])
+    prm = spec.params
+    n_outer = 2
+    t = time.perf_counter()
+    _, log = sb.sb_recon(y, p["sens"], p["mask"], prm.mu, prm.lam, prm.gamma, n_outer, 1,
+                         prm.wavelet_levels, prm.eps, prm.max_iters, "circulant" if precond else "none")
+    dt = time.perf_counter() - t
+    it = sum(log.pcg_iters)
+    return {"value": it / dt, "unit": "PCG iters/s", "cores": 1, "kind": "oracle",
+            "sample": f"{n_outer} SB outer iterations of slice 0 ({it} PCG iterations, {dt:.1f} s), "
+                      f"numpy fp64 single thread; sb_recon time extrapolates to "
+                      f"{dt / n_outer * prm.n_outer:.1f} s for {prm.n_outer} outer"}
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_setup()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    from paper_1710_01758_b200 import SbPcg
+
+    spec, per, first = workload(args.config, ws, rank, args.slices)
+    prm = spec.params
+    phantom, sens, mask, noise = make_inputs(args.config, first, per)
+    sens_d = torch.from_numpy(sens).to(torch.complex64).to(dev)
+    mask_d = torch.from_numpy(mask).to(dev)
+    ctx = SbPcg(sens_d, mask_d, prm.mu, prm.lam, prm.gamma, prm.wavelet_levels)
+    # k-space y = R (F S x + sigma n), sigma = 0.005 max|F S x| (reading A21), on the GPU
+    x_d = torch.from_numpy(phantom).to(torch.complex64).to(dev)
+    yfull = ctx.encode(x_d, full=True)
+    sigma = 0.005 * yfull.abs().amax(dim=(1, 2, 3), keepdim=True)
+    mask_c = mask_d.to(torch.complex64).unsqueeze(1)
+    y_d = (mask_c * (yfull + sigma * torch.from_numpy(noise).to(torch.complex64).to(dev))).contiguous()
+    del yfull
+    out = torch.empty((per, spec.shape[0], spec.shape[1]), dtype=torch.complex64, device=dev)
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+    use_graph = not args.no_graph
+
+    def step():
+        ctx.build_precond()
+        _, log = ctx.recon(y_d, prm.n_outer, eps=prm.eps, max_iters=prm.max_iters,
+                           precond=args.precond, use_graph=use_graph, out=out)
+        return log
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clock = ClockSampler(dev.index)
+    clock.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    total_ms = 0.0
+    iters = 0
+    l0 = ctx.launches()
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flush between timed steps (inputs < L2 at config 2)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        log = step()
+        e1.record(st)
+        e1.synchronize()
+        total_ms += e0.elapsed_time(e1)
+        iters += sum(sum(r) for r in log["pcg_iters"])
+    torch.cuda.synchronize()
+    launches = ctx.launches() - l0
+    if dist:
+        dist.barrier()
+    # clock probe: keep the GPU loaded ~1.5 s so the sampler sees the steady state
+    t_end = time.perf_counter() + 1.5
+    while time.perf_counter() < t_end:
+        step()
+    torch.cuda.synchronize()
+    clocks = clock.stop()
+
+    # max over ranks of the device time; sum of work
+    t_max = total_ms
+    it_sum = iters
+    if dist:
+        tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+        ii = torch.tensor([iters], device=dev, dtype=torch.float64)
+        dist.all_reduce(ii, op=dist.ReduceOp.SUM)
+        it_sum = int(ii.item())
+    value = it_sum / (t_max / 1e3)
+    ms_per_step = t_max / args.steps
+
+    # ---- dominant-kernel roofline: K1 (fused matvec) timed with CUDA events per launch on the
+    # context stream (eager mode for this pass)
+    ctx.set_kernel_timing(True)
+    for _ in range(max(1, min(args.steps, 5))):
+        flush.fill_(1.0)
+        step()
+    torch.cuda.synchronize()
+    k_ms, k_n, k_bytes = ctx.kernel_time(0)
+    ctx.set_kernel_timing(False)
+    peak, peak_kind = peaks()
+    k_avg_s = (k_ms / max(k_n, 1)) / 1e3
+    achieved = k_bytes / k_avg_s / 1e9 if k_avg_s > 0 else 0.0
+    traffic = load_traffic(args.config)
+
+    # ---- e2e: public API with HOST (pinned) buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        sens_h = torch.from_numpy(sens).to(torch.complex64).pin_memory()
+        mask_h = torch.from_numpy(mask).pin_memory()
+        y_h = y_d.cpu().pin_memory()
+        x_h = torch.empty((per,) + tuple(spec.shape), dtype=torch.complex64).pin_memory()
+
+        def e2e_step():
+            c2 = SbPcg(sens_h, mask_h, prm.mu, prm.lam, prm.gamma, prm.wavelet_levels)
+            _, lg = c2.recon(y_h, prm.n_outer, eps=prm.eps, max_iters=prm.max_iters,
+                             precond=args.precond, use_graph=use_graph, out=x_h)
+            c2.close()
+            return lg
+        for _ in range(min(args.warmup, 3)):
+            e2e_step()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e_it = 0
+        for _ in range(args.steps):
+            lg = e2e_step()
+            e_it += sum(sum(r) for r in lg["pcg_iters"])
+        torch.cuda.synchronize()
+        e_dt = time.perf_counter() - t0
+        if dist:
+            tt = torch.tensor([e_dt, e_it], device=dev, dtype=torch.float64)
+            mx = tt.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+            e_dt, e_it = float(mx[0].item()), float(tt[1].item())
+        h2d = sens_h.numel() * 8 + mask_h.numel() + y_h.numel() * 8
+        e2e = {"value": e_it / e_dt, "unit": "PCG iters/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(x_h.numel() * 8),
+               "ms_per_step": 1e3 * e_dt / args.steps}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(args.config, args.precond)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "PCG iters/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak" if args.config != 3 else "strong",
+            "vs_baseline": None, "dtype": "c64 (fp32 complex; Lambda built in f64)",
+            "data": "synthetic (seeded phantoms, coil maps, masks; k-space by sb_encode)",
+            "config": {"workload": spec.name, "problems_per_gpu": per, "shape": list(spec.shape),
+                       "coils": spec.coils, "mask": "VD lines R=%d, %d-line centre" % (spec.accel, spec.center),
+                       "mu": prm.mu, "lambda": prm.lam, "gamma": prm.gamma, "n_outer": prm.n_outer,
+                       "pcg_eps": prm.eps, "pcg_max_iters": prm.max_iters,
+                       "precond": "circulant" if args.precond else "none",
+                       "pcg_iters_per_step": it_sum / args.steps / ws,
+                       "sb_recon_ms": ms_per_step, "l2": "flushed between timed steps (256 MiB write)",
+                       "loop": "CUDA graph, conditional while node" if use_graph else "eager"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "k1_matvec (fused coil FFT matvec)",
+                         "kernel_avg_us": k_avg_s * 1e6, "kernel_launches_timed": k_n,
+                         "alg_bytes_per_launch": k_bytes},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+    ctx.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

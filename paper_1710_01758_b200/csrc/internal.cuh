@@ -65,10 +65,20 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // Deterministic block sum (fixed shuffle tree, fixed warp order).  All threads call it;
-// result valid in thread 0.  `red` must hold >= 32 doubles.
+// result valid in thread 0.  `red` must hold >= 32 doubles.  Blocks smaller than a warp
+// (tiny images) take a serial shared-memory path: shuffles need every lane present.
 __device__ __forceinline__ double block_sum(double v, double* red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nw = (blockDim.x + 31) >> 5;
+  if (blockDim.x & 31) {
+    __syncthreads();
+    red[threadIdx.x] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+      for (int i = 0; i < (int)blockDim.x; ++i) s += red[i];
+    return s;
+  }
+  const int nw = blockDim.x >> 5;
   v = warp_sum(v);
   __syncthreads();
   if (lane == 0) red[wid] = v;
@@ -81,9 +91,16 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
-// Sum n partials in a fixed order using one warp (lane i takes i, i+32, ...; then a fixed
-// shuffle tree).  Result valid in all lanes of the calling warp.
+// Sum n partials in a fixed order using the first warp (lane i takes i, i+32, ...; then a
+// fixed shuffle tree).  Call from threads 0..31 (or all threads of a sub-warp block);
+// result valid in thread 0.
 __device__ __forceinline__ double warp_sum_partials(const double* p, int n) {
+  if (blockDim.x < 32) {
+    double s = 0.0;
+    if (threadIdx.x == 0)
+      for (int i = 0; i < n; ++i) s += __ldcg(p + i);
+    return s;
+  }
   const int lane = threadIdx.x & 31;
   double s = 0.0;
   for (int i = lane; i < n; i += 32) s += __ldcg(p + i);
@@ -106,6 +123,15 @@ __device__ __forceinline__ bool publish_and_check_last(double v0, double v1, con
   if (last) __threadfence();
   return last;
 }
+
+// ------------------------------------------------------------------ programmatic dependent launch
+// Every kernel of the PCG loop is launched with cudaLaunchAttributeProgrammaticStreamSerialization:
+// it may start while its predecessor drains, does its constant setup (twiddles, masks, TMA of
+// the constant coil maps), then waits for the predecessor grid (griddepcontrol.wait) before
+// touching anything the predecessor produced.  Every CTA executes pdl_wait() before exiting,
+// so completion stays transitive along the chain.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ------------------------------------------------------------------ mbarrier / TMA (sm_90+)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

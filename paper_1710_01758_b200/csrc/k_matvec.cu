@@ -56,20 +56,8 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
   const size_t img = (size_t)M * N;
   const size_t boff = (size_t)b * img;
 
-  int pidx = 0;
-  double beta = 0.0, alpha_prev = 0.0;
-  bool first = true;
-  if constexpr (MODE == K1_PCG) {
-    const Scal& s = a.L.scal[b];
-    if (!s.active) return;  // uniform over the cluster (same problem)
-    const int k = s.iter + 1;  // iteration being formed
-    first = (k == 1);
-    pidx = k & 1;
-    beta = s.beta;
-    alpha_prev = s.alpha;
-  }
-
-  // ---- setup: barriers, twiddles, mask
+  // ---- setup on constant data (overlaps the predecessor kernel under PDL): barriers,
+  // twiddles, mask, and the TMA of the first two coil-map tiles (coil maps never change)
   const int ncoil = (a.C - g + G - 1) / G;  // coils g, g+G, ...
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -88,37 +76,93 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
       tma_load_3d(ring + s * TILE, &tmap, 2 * col0, 0, b * a.C + c, &bar[s]);
     }
   }
+  pdl_trigger();
+  pdl_wait();
 
-  // ---- prologue: the p tile (+halo); PCG forms p_k = z + beta p_{k-1} and x += alpha p_{k-1}
+  int pidx = 0;
+  double beta = 0.0, alpha_prev = 0.0;
+  bool first = true;
+  if constexpr (MODE == K1_PCG) {
+    const Scal& s = a.L.scal[b];
+    if (!s.active) {  // uniform over the cluster (same problem): drain the TMAs, leave
+      for (int st = 0; st < 2 && st < ncoil; ++st) mbar_wait(&bar[st], 0);
+      return;
+    }
+    const int k = s.iter + 1;  // iteration being formed
+    first = (k == 1);
+    pidx = k & 1;
+    beta = s.beta;
+    alpha_prev = s.alpha;
+  }
+
+  // ---- prologue: the p tile (+halo) into shared memory.  Loads are issued in batches
+  // with no global store in between (the x / p_k stores follow in phase 2), so they overlap.
+  // PCG forms p_k = z + beta p_{k-1} (standard PCG) and x += alpha p_{k-1}.
   const int rows_per = M / G;
-  const int r0 = g * rows_per, r1 = r0 + rows_per;
-  for (int e = tid; e < M * PW; e += NT) {
-    const int row = e / PW, cc = e % PW;
-    const int gcol = (col0 + cc - 1 + N) % N;
-    const size_t gi = boff + (size_t)row * N + gcol;
-    float2 p;
-    if constexpr (MODE == K1_PCG) {
-      const float2 zz = a.z[gi];
-      if (first) {
-        p = zz;
-      } else {
-        const float2* pold = pidx ? a.pbuf0 : a.pbuf1;
-        const float2 po = pold[gi];
-        p = make_float2(zz.x + (float)beta * po.x, zz.y + (float)beta * po.y);
-        if (cc >= 1 && cc <= W && row >= r0 && row < r1) {
-          float2 xv = a.x[gi];
-          xv.x += (float)alpha_prev * po.x;
-          xv.y += (float)alpha_prev * po.y;
-          a.x[gi] = xv;
+  const int r0 = g * rows_per;
+  constexpr int PE = (M * PW + NT - 1) / NT;  // elements per thread
+  constexpr int CH = PE < 10 ? PE : 10;
+  const float2* pold = pidx ? a.pbuf0 : a.pbuf1;
+  float2* pnew = pidx ? a.pbuf1 : a.pbuf0;
+  const bool need_old = (MODE == K1_PCG) && !first;
+  for (int c0 = 0; c0 < PE; c0 += CH) {
+    float2 zz[CH], po[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int e = (c0 + i) * NT + tid;
+      zz[i] = make_float2(0.f, 0.f);
+      po[i] = make_float2(0.f, 0.f);
+      if (c0 + i < PE && e < M * PW) {
+        const int row = e / PW, cc = e % PW;
+        int gcol = col0 + cc - 1;
+        gcol = gcol < 0 ? gcol + N : (gcol >= N ? gcol - N : gcol);
+        const size_t gi = boff + (size_t)row * N + gcol;
+        if constexpr (MODE == K1_PCG) {
+          zz[i] = a.z[gi];
+          if (need_old) po[i] = pold[gi];
+        } else {
+          zz[i] = a.vin[gi];
         }
       }
-      if (cc >= 1 && cc <= W && row >= r0 && row < r1) (pidx ? a.pbuf1 : a.pbuf0)[gi] = p;
-    } else {
-      p = a.vin[gi];
     }
-    pt[e] = p;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int e = (c0 + i) * NT + tid;
+      if (c0 + i < PE && e < M * PW)
+        pt[e] = need_old ? make_float2(zz[i].x + (float)beta * po[i].x, zz[i].y + (float)beta * po[i].y) : zz[i];
+    }
   }
   __syncthreads();
+  if constexpr (MODE == K1_PCG) {
+    // phase 2: this CTA's rows x W columns: p_k -> pnew, x += alpha_{k-1} p_{k-1}
+    constexpr int OE = (M * W + NT - 1) / NT;  // upper bound of own elements per thread
+    const int own = rows_per * W;
+    constexpr int CH2 = OE < 8 ? OE : 8;
+    for (int c0 = 0; c0 < OE; c0 += CH2) {
+      float2 xv[CH2], po[CH2];
+#pragma unroll
+      for (int i = 0; i < CH2; ++i) {
+        const int e = (c0 + i) * NT + tid;
+        if (need_old && c0 + i < OE && e < own) {
+          const size_t gi = boff + (size_t)(r0 + e / W) * N + col0 + e % W;
+          xv[i] = a.x[gi];
+          po[i] = pold[gi];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < CH2; ++i) {
+        const int e = (c0 + i) * NT + tid;
+        if (c0 + i < OE && e < own) {
+          const int row = r0 + e / W, cc = e % W;
+          const size_t gi = boff + (size_t)row * N + col0 + cc;
+          pnew[gi] = pt[row * PW + cc + 1];
+          if (need_old) {
+            a.x[gi] = make_float2(xv[i].x + (float)alpha_prev * po[i].x, xv[i].y + (float)alpha_prev * po[i].y);
+          }
+        }
+      }
+    }
+  }
 
   // ---- coil loop
   float2 acc[N1];
@@ -184,51 +228,70 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
   if (G > 1) cluster.sync(); else __syncthreads();
 
   double d0 = 0.0, d1 = 0.0;
-  for (int e = tid; e < rows_per * W; e += NT) {
-    const int row = r0 + e / W, cc = e % W;
-    float2 av = make_float2(0.f, 0.f);
-    for (int gg = 0; gg < G; ++gg) {
-      const float2* src = (gg == g) ? accb : cluster.map_shared_rank(accb, gg);
-      const float2 t = src[row * W + cc];
-      av.x += t.x;
-      av.y += t.y;
-    }
-    const float2 p = pt[row * PW + cc + 1];
-    const float2 pu = pt[((row + M - 1) % M) * PW + cc + 1];
-    const float2 pd = pt[((row + 1) % M) * PW + cc + 1];
-    const float2 pl = pt[row * PW + cc];
-    const float2 pr = pt[row * PW + cc + 2];
-    const float2 lp = make_float2(4.f * p.x - pu.x - pd.x - pl.x - pr.x,
-                                  4.f * p.y - pu.y - pd.y - pl.y - pr.y);
-    const size_t gi = boff + (size_t)row * N + col0 + cc;
-    const float2 reg = make_float2(a.lam * lp.x + a.gam * p.x, a.lam * lp.y + a.gam * p.y);
+  constexpr int EE = (M * W + NT - 1) / NT;  // upper bound of epilogue elements per thread
+  constexpr int CH3 = EE < 8 ? EE : 8;
+  const int nep = rows_per * W;
+  for (int c0 = 0; c0 < EE; c0 += CH3) {
+    float2 lb[CH3], lu[CH3], lu1[CH3], lr[CH3];
     if constexpr (MODE == K1_RESID) {
-      float2 bb;
-      if (a.bvec != nullptr) {
-        bb = a.bvec[gi];
-      } else {
-        float2 uu = a.u[gi];
-        if (a.update_u) {
-          const float2 u1 = a.u1[gi];
-          uu = make_float2(uu.x + u1.x - av.x, uu.y + u1.y - av.y);
-          a.u[gi] = uu;
+#pragma unroll
+      for (int i = 0; i < CH3; ++i) {
+        const int e = (c0 + i) * NT + tid;
+        if (c0 + i < EE && e < nep) {
+          const size_t gi = boff + (size_t)(r0 + e / W) * N + col0 + e % W;
+          if (a.bvec != nullptr) {
+            lb[i] = a.bvec[gi];
+          } else {
+            lu[i] = a.u[gi];
+            lu1[i] = a.update_u ? a.u1[gi] : make_float2(0.f, 0.f);
+            lr[i] = a.rhs_reg != nullptr ? a.rhs_reg[gi] : make_float2(0.f, 0.f);
+          }
         }
-        bb = make_float2(a.mu * uu.x, a.mu * uu.y);
-        if (a.rhs_reg != nullptr) {
-          const float2 rr = a.rhs_reg[gi];
-          bb.x += rr.x;
-          bb.y += rr.y;
-        }
-        a.bout[gi] = bb;
       }
-      const float2 r = make_float2(bb.x - (a.mu * av.x + reg.x), bb.y - (a.mu * av.y + reg.y));
-      a.out[gi] = r;
-      d0 += (double)bb.x * bb.x + (double)bb.y * bb.y;
-      d1 += (double)r.x * r.x + (double)r.y * r.y;
-    } else {
-      const float2 q = make_float2(a.mu * av.x + reg.x, a.mu * av.y + reg.y);
-      a.out[gi] = q;
-      d0 += (double)p.x * q.x + (double)p.y * q.y;
+    }
+#pragma unroll
+    for (int i = 0; i < CH3; ++i) {
+      const int e = (c0 + i) * NT + tid;
+      if (!(c0 + i < EE && e < nep)) continue;
+      const int row = r0 + e / W, cc = e % W;
+      float2 av = make_float2(0.f, 0.f);
+      for (int gg = 0; gg < G; ++gg) {
+        const float2* src = (gg == g) ? accb : cluster.map_shared_rank(accb, gg);
+        const float2 t = src[row * W + cc];
+        av.x += t.x;
+        av.y += t.y;
+      }
+      const float2 p = pt[row * PW + cc + 1];
+      const float2 pu = pt[((row + M - 1) % M) * PW + cc + 1];
+      const float2 pd = pt[((row + 1) % M) * PW + cc + 1];
+      const float2 pl = pt[row * PW + cc];
+      const float2 pr = pt[row * PW + cc + 2];
+      const float2 lp = make_float2(4.f * p.x - pu.x - pd.x - pl.x - pr.x,
+                                    4.f * p.y - pu.y - pd.y - pl.y - pr.y);
+      const size_t gi = boff + (size_t)row * N + col0 + cc;
+      const float2 reg = make_float2(a.lam * lp.x + a.gam * p.x, a.lam * lp.y + a.gam * p.y);
+      if constexpr (MODE == K1_RESID) {
+        float2 bb;
+        if (a.bvec != nullptr) {
+          bb = lb[i];
+        } else {
+          float2 uu = lu[i];
+          if (a.update_u) {
+            uu = make_float2(uu.x + lu1[i].x - av.x, uu.y + lu1[i].y - av.y);
+            a.u[gi] = uu;
+          }
+          bb = make_float2(a.mu * uu.x + lr[i].x, a.mu * uu.y + lr[i].y);
+          a.bout[gi] = bb;
+        }
+        const float2 r = make_float2(bb.x - (a.mu * av.x + reg.x), bb.y - (a.mu * av.y + reg.y));
+        a.out[gi] = r;
+        d0 += (double)bb.x * bb.x + (double)bb.y * bb.y;
+        d1 += (double)r.x * r.x + (double)r.y * r.y;
+      } else {
+        const float2 q = make_float2(a.mu * av.x + reg.x, a.mu * av.y + reg.y);
+        a.out[gi] = q;
+        d0 += (double)p.x * q.x + (double)p.y * q.y;
+      }
     }
   }
   if (G > 1) cluster.sync();  // peers finished reading this CTA's accb
@@ -269,19 +332,7 @@ static cudaError_t launch_k1_t(const K1Args& a, const CUtensorMap* tmap, int G, 
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(G, a.N / W, a.B);
-  cfg.blockDim = dim3(Split<M>::N2 * W);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = G;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, *tmap, a);
+  return launch_ex(kern, dim3(G, a.N / W, a.B), dim3(Split<M>::N2 * W), smem, st, G, *tmap, a);
 }
 
 template <int M, int W>
@@ -321,7 +372,7 @@ int k1_default_W(int M, int N) { return (N % 8 == 0) ? 8 : 4; }
 
 cudaError_t launch_k1(int mode, bool separable, const K1Args& a, const CUtensorMap* tmap, int W, int G,
                       cudaStream_t st) {
-  if (a.M % G != 0 || a.N % W != 0) return cudaErrorInvalidValue;
+  if (a.M % G != 0 || a.N % W != 0 || G > 8) return cudaErrorInvalidValue;
   switch (a.M) {
     case 8: return launch_k1_m<8>(mode, separable, a, tmap, W, G, st);
     case 16: return launch_k1_m<16>(mode, separable, a, tmap, W, G, st);

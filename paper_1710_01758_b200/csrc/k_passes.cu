@@ -14,20 +14,20 @@
 
 namespace sbk {
 
-constexpr int PW_COL = 8;  // columns per column-pass CTA
-
-template <int M>
+// columns per column-pass CTA: 8 normally, 2 when the grid would not fill the SMs
+template <int M, int W_>
 struct ColCfg {
-  static constexpr int W = PW_COL;
+  static constexpr int W = W_;
   static constexpr int N1 = Split<M>::N1, N2 = Split<M>::N2, NT = N2 * W;
   using Lay = typename ColLayout<M, W>::L;
   static constexpr int XS = ColLayout<M, W>::size;
 };
 
-template <int N>
+// rows per row-pass CTA: 256 threads normally, one warp when the grid would not fill the SMs
+template <int N, int LINES_>
 struct RowCfg {
   static constexpr int N1 = Split<N>::N1, N2 = Split<N>::N2;
-  static constexpr int LINES = (256 / N2) > 0 ? (256 / N2) : 1;
+  static constexpr int LINES = LINES_;
   static constexpr int NT = LINES * N2;
   using Lay = typename RowLayout<N, LINES>::L;
   static constexpr int XS = RowLayout<N, LINES>::size;
@@ -38,9 +38,9 @@ __device__ __forceinline__ bool slice_active(const PassArgs& a, int b) {
 }
 
 // ------------------------------------------------------------------ column passes
-template <int M, int KIND>
-__global__ void __launch_bounds__(ColCfg<M>::NT) k_col(const PassArgs a) {
-  using C = ColCfg<M>;
+template <int M, int W_, int KIND>
+__global__ void __launch_bounds__(ColCfg<M, W_>::NT) k_col(const PassArgs a) {
+  using C = ColCfg<M, W_>;
   constexpr int N1 = C::N1, W = C::W, NT = C::NT;
   __shared__ __align__(16) float2 xch[C::XS];
   __shared__ float2 tw[M];
@@ -60,6 +60,9 @@ __global__ void __launch_bounds__(ColCfg<M>::NT) k_col(const PassArgs a) {
     b = blockIdx.y;
   }
   const size_t boff = (size_t)b * img;
+  for (int i = tid; i < M; i += NT) tw[i] = a.tw_m[i];
+  pdl_trigger();
+  pdl_wait();
 
   if constexpr (KIND == P_PRE_A_FWD_COL || KIND == P_PRE_C_INV_COL || KIND == P_GEN_A_COL) {
     if (!slice_active(a, b)) {
@@ -69,7 +72,6 @@ __global__ void __launch_bounds__(ColCfg<M>::NT) k_col(const PassArgs a) {
       return;
     }
   }
-  for (int i = tid; i < M; i += NT) tw[i] = a.tw_m[i];
   __syncthreads();
 
   float2 v[N1];
@@ -78,18 +80,23 @@ __global__ void __launch_bounds__(ColCfg<M>::NT) k_col(const PassArgs a) {
   if constexpr (KIND == P_PRE_A_FWD_COL) {
     // mode 1 (PCG): r_k = r_{k-1} - alpha_k q_k ; mode 0 (init): r given
     const double alpha = (a.mode == 1) ? a.L.scal[b].alpha : 0.0;
+    // all loads first (r is updated in place: no store may precede a load)
+    float2 qv[N1];
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) {
       const size_t gi = boff + (size_t)natidx<M>(j, n1) * N + col;
-      float2 r = a.a0[gi];
-      if (a.mode == 1) {
-        const float2 q = a.a1[gi];
-        r.x -= (float)alpha * q.x;
-        r.y -= (float)alpha * q.y;
-        a.o0[gi] = r;
-        d0 += (double)r.x * r.x + (double)r.y * r.y;
+      v[n1] = a.a0[gi];
+      qv[n1] = (a.mode == 1) ? a.a1[gi] : make_float2(0.f, 0.f);
+    }
+    if (a.mode == 1) {
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) {
+        const size_t gi = boff + (size_t)natidx<M>(j, n1) * N + col;
+        v[n1].x -= (float)alpha * qv[n1].x;
+        v[n1].y -= (float)alpha * qv[n1].y;
+        a.o0[gi] = v[n1];
+        d0 += (double)v[n1].x * v[n1].x + (double)v[n1].y * v[n1].y;
       }
-      v[n1] = r;
     }
     fft_fwd<M, typename C::Lay>(v, xch, tw, j, l);
 #pragma unroll
@@ -108,17 +115,18 @@ __global__ void __launch_bounds__(ColCfg<M>::NT) k_col(const PassArgs a) {
       }
     }
   } else if constexpr (KIND == P_PRE_C_INV_COL) {
+    float2 rv[N1];
 #pragma unroll
-    for (int s = 0; s < N1; ++s) v[s] = a.tmp[boff + (size_t)specidx<M>(j, s) * N + col];
+    for (int s = 0; s < N1; ++s) {
+      v[s] = a.tmp[boff + (size_t)specidx<M>(j, s) * N + col];
+      rv[s] = (a.mode >= 0) ? a.a0[boff + (size_t)natidx<M>(j, s) * N + col] : make_float2(0.f, 0.f);
+    }
     fft_inv<M, typename C::Lay>(v, xch, tw, j, l);
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) {
       const size_t gi = boff + (size_t)natidx<M>(j, n1) * N + col;
       a.o0[gi] = v[n1];
-      if (a.mode >= 0) {
-        const float2 r = a.a0[gi];
-        d0 += (double)r.x * v[n1].x + (double)r.y * v[n1].y;
-      }
+      d0 += (double)rv[n1].x * v[n1].x + (double)rv[n1].y * v[n1].y;
     }
     if (a.mode >= 0) {
       const double s0 = block_sum(d0, red);
@@ -181,13 +189,17 @@ __global__ void __launch_bounds__(ColCfg<M>::NT) k_col(const PassArgs a) {
     for (int cc = 0; cc < a.C; ++cc) {
       const float2* t = a.tmp + ((size_t)b * a.C + cc) * img;
       const float2* sc = a.sens + ((size_t)b * a.C + cc) * img;
+      float2 sv[N1];
 #pragma unroll
-      for (int s = 0; s < N1; ++s) v[s] = t[(size_t)specidx<M>(j, s) * N + col];
+      for (int s = 0; s < N1; ++s) {
+        v[s] = t[(size_t)specidx<M>(j, s) * N + col];
+        sv[s] = sc[(size_t)natidx<M>(j, s) * N + col];
+      }
       fft_inv<M, typename C::Lay>(v, xch, tw, j, l);
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) {
         const float2 vv = make_float2(v[n1].x * a.scale, v[n1].y * a.scale);
-        const float2 s = sc[(size_t)natidx<M>(j, n1) * N + col];
+        const float2 s = sv[n1];
         const float2 u = cmulc(s, vv);
         acc[n1].x += u.x;
         acc[n1].y += u.y;
@@ -205,9 +217,9 @@ __global__ void __launch_bounds__(ColCfg<M>::NT) k_col(const PassArgs a) {
 }
 
 // ------------------------------------------------------------------ row passes
-template <int N, int KIND>
-__global__ void __launch_bounds__(RowCfg<N>::NT) k_row(const PassArgs a) {
-  using R = RowCfg<N>;
+template <int N, int LINES_, int KIND>
+__global__ void __launch_bounds__(RowCfg<N, LINES_>::NT) k_row(const PassArgs a) {
+  using R = RowCfg<N, LINES_>;
   constexpr int N1 = R::N1, N2 = R::N2, LINES = R::LINES, NT = R::NT;
   __shared__ __align__(16) float2 xch[R::XS];
   __shared__ float2 tw[N];
@@ -215,6 +227,9 @@ __global__ void __launch_bounds__(RowCfg<N>::NT) k_row(const PassArgs a) {
   const int M = a.M;
   const int row = blockIdx.x * LINES + line;
   const size_t img = (size_t)M * N;
+  for (int i = tid; i < N; i += NT) tw[i] = a.tw_n[i];
+  pdl_trigger();
+  pdl_wait();
   int b, c = 0;
   if constexpr (KIND == P_PRE_B_ROW) {
     b = blockIdx.y;
@@ -226,7 +241,6 @@ __global__ void __launch_bounds__(RowCfg<N>::NT) k_row(const PassArgs a) {
       if (a.mode == 1 && !slice_active(a, b)) return;
     }
   }
-  for (int i = tid; i < N; i += NT) tw[i] = a.tw_n[i];
   __syncthreads();
   const bool in_range = row < M;
   const int rr = in_range ? row : M - 1;  // keep barriers uniform
@@ -235,14 +249,15 @@ __global__ void __launch_bounds__(RowCfg<N>::NT) k_row(const PassArgs a) {
   if constexpr (KIND == P_PRE_B_ROW) {
     float2* t = a.tmp + (size_t)b * img + (size_t)rr * N;
     const float* li = a.lam_inv + (size_t)b * a.lam_bstride + (size_t)rr * N;
+    float lv[N1];
 #pragma unroll
-    for (int n1 = 0; n1 < N1; ++n1) v[n1] = t[natidx<N>(j, n1)];
+    for (int n1 = 0; n1 < N1; ++n1) {
+      v[n1] = t[natidx<N>(j, n1)];
+      lv[n1] = li[specidx<N>(j, n1)];
+    }
     fft_fwd<N, typename R::Lay>(v, xch, tw, j, line);
 #pragma unroll
-    for (int s = 0; s < N1; ++s) {
-      const float f = li[specidx<N>(j, s)];
-      v[s] = make_float2(v[s].x * f, v[s].y * f);
-    }
+    for (int s = 0; s < N1; ++s) v[s] = make_float2(v[s].x * lv[s], v[s].y * lv[s]);
     fft_inv<N, typename R::Lay>(v, xch, tw, j, line);
     if (in_range) {
 #pragma unroll
@@ -302,6 +317,8 @@ __global__ void __launch_bounds__(RowCfg<N>::NT) k_row(const PassArgs a) {
 __global__ void __launch_bounds__(256) k_nopre(const PassArgs a) {
   __shared__ double red[32];
   __shared__ int lastflag;
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.y;
   const size_t img = (size_t)a.M * a.N;
   if (!slice_active(a, b)) {
@@ -310,17 +327,30 @@ __global__ void __launch_bounds__(256) k_nopre(const PassArgs a) {
   }
   const double alpha = (a.mode == 1) ? a.L.scal[b].alpha : 0.0;
   double d0 = 0.0;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < img; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t gi = (size_t)b * img + i;
-    float2 r = a.a0[gi];
-    if (a.mode == 1) {
-      const float2 q = a.a1[gi];
-      r.x -= (float)alpha * q.x;
-      r.y -= (float)alpha * q.y;
-      a.o0[gi] = r;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < img; i0 += 4 * stride) {
+    float2 r[4], q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const size_t i = i0 + u * stride;
+      if (i < img) {
+        r[u] = a.a0[(size_t)b * img + i];
+        q[u] = (a.mode == 1) ? a.a1[(size_t)b * img + i] : make_float2(0.f, 0.f);
+      }
     }
-    a.o1[gi] = r;  // z = r
-    d0 += (double)r.x * r.x + (double)r.y * r.y;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const size_t i = i0 + u * stride;
+      if (i >= img) continue;
+      const size_t gi = (size_t)b * img + i;
+      if (a.mode == 1) {
+        r[u].x -= (float)alpha * q[u].x;
+        r[u].y -= (float)alpha * q[u].y;
+        a.o0[gi] = r[u];
+      }
+      a.o1[gi] = r[u];  // z = r
+      d0 += (double)r[u].x * r[u].x + (double)r[u].y * r[u].y;
+    }
   }
   const double s0 = block_sum(d0, red);
   const int nblk = gridDim.x;
@@ -343,6 +373,8 @@ __global__ void __launch_bounds__(256) k_nopre(const PassArgs a) {
 
 // PCG exit: x += alpha_K p_K (the last completed iteration), or x = 0 when ||b|| = 0.
 __global__ void __launch_bounds__(256) k_fixup(const PassArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.y;
   const Scal& s = a.L.scal[b];
   const size_t img = (size_t)a.M * a.N;
@@ -352,22 +384,31 @@ __global__ void __launch_bounds__(256) k_fixup(const PassArgs a) {
   if (!zero && !upd) return;
   const float alpha = (float)s.alpha;
   const float2* p = (K & 1) ? a.pbuf1 : a.pbuf0;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < img; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t gi = (size_t)b * img + i;
-    if (zero) {
-      a.x[gi] = make_float2(0.f, 0.f);
-    } else {
-      float2 xv = a.x[gi];
-      const float2 pv = p[gi];
-      xv.x += alpha * pv.x;
-      xv.y += alpha * pv.y;
-      a.x[gi] = xv;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < img; i0 += 4 * stride) {
+    float2 xv[4], pv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const size_t i = i0 + u * stride;
+      if (i < img && !zero) {
+        xv[u] = a.x[(size_t)b * img + i];
+        pv[u] = p[(size_t)b * img + i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const size_t i = i0 + u * stride;
+      if (i >= img) continue;
+      a.x[(size_t)b * img + i] = zero ? make_float2(0.f, 0.f)
+                                      : make_float2(xv[u].x + alpha * pv[u].x, xv[u].y + alpha * pv[u].y);
     }
   }
 }
 
 // Recon log row for this solve, then advance the solve index (one thread).
 __global__ void k_log(const Loop L) {
+  pdl_trigger();
+  pdl_wait();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const int slot = L.ctl->solve_idx;
   for (int b = 0; b < L.B; ++b) {
@@ -379,24 +420,34 @@ __global__ void k_log(const Loop L) {
 }
 
 cudaError_t launch_log(const Loop& L, cudaStream_t st) {
-  k_log<<<1, 32, 0, st>>>(L);
-  return cudaGetLastError();
+  return launch_ex(k_log, dim3(1), dim3(32), 0, st, 0, L);
 }
 
 // ------------------------------------------------------------------ dispatch
+// Narrow tiles (more, smaller CTAs) when the batch is too small to fill 148 SMs.
+constexpr int kFill = 2 * 148;
+
 template <int M, int KIND>
 static cudaError_t launch_col_t(const PassArgs& a, cudaStream_t st) {
-  int nimg = (KIND == P_ENC_COL || KIND == P_GEN_A_COL) ? a.B * a.C : a.B;
-  dim3 grid(a.N / PW_COL, nimg);
-  k_col<M, KIND><<<grid, ColCfg<M>::NT, 0, st>>>(a);
-  return cudaGetLastError();
+  const int nimg = (KIND == P_ENC_COL || KIND == P_GEN_A_COL) ? a.B * a.C : a.B;
+  constexpr int WS = (32 / Split<M>::N2) > 2 ? 32 / Split<M>::N2 : 2;  // >= one warp per CTA
+  if (WS < 8 && (a.N / 8) * nimg < kFill) {
+    return launch_ex(k_col<M, (WS < 8 ? WS : 8), KIND>, dim3(a.N / WS, nimg), dim3(ColCfg<M, (WS < 8 ? WS : 8)>::NT),
+                     0, st, 0, a);
+  }
+  return launch_ex(k_col<M, 8, KIND>, dim3(a.N / 8, nimg), dim3(ColCfg<M, 8>::NT), 0, st, 0, a);
 }
 template <int N, int KIND>
 static cudaError_t launch_row_t(const PassArgs& a, cudaStream_t st) {
-  int nimg = (KIND == P_PRE_B_ROW) ? a.B : a.B * a.C;
-  dim3 grid((a.M + RowCfg<N>::LINES - 1) / RowCfg<N>::LINES, nimg);
-  k_row<N, KIND><<<grid, RowCfg<N>::NT, 0, st>>>(a);
-  return cudaGetLastError();
+  const int nimg = (KIND == P_PRE_B_ROW) ? a.B : a.B * a.C;
+  constexpr int LBIG = (256 / Split<N>::N2) > 0 ? 256 / Split<N>::N2 : 1;
+  constexpr int LSMALL = (32 / Split<N>::N2) > 0 ? 32 / Split<N>::N2 : 1;
+  if (((a.M + LBIG - 1) / LBIG) * nimg < kFill) {
+    using R = RowCfg<N, LSMALL>;
+    return launch_ex(k_row<N, LSMALL, KIND>, dim3((a.M + LSMALL - 1) / LSMALL, nimg), dim3(R::NT), 0, st, 0, a);
+  }
+  using R = RowCfg<N, LBIG>;
+  return launch_ex(k_row<N, LBIG, KIND>, dim3((a.M + LBIG - 1) / LBIG, nimg), dim3(R::NT), 0, st, 0, a);
 }
 
 template <int KIND>
@@ -444,14 +495,12 @@ cudaError_t launch_pass(int kind, const PassArgs& a, cudaStream_t st) {
     case P_NOPRE: {
       int nb = (int)((img + 2047) / 2048);
       if (nb > 64) nb = 64;
-      k_nopre<<<dim3(nb, a.B), 256, 0, st>>>(a);
-      return cudaGetLastError();
+      return launch_ex(k_nopre, dim3(nb, a.B), dim3(256), 0, st, 0, a);
     }
     case P_FIXUP: {
       int nb = (int)((img + 1023) / 1024);
       if (nb > 256) nb = 256;
-      k_fixup<<<dim3(nb, a.B), 256, 0, st>>>(a);
-      return cudaGetLastError();
+      return launch_ex(k_fixup, dim3(nb, a.B), dim3(256), 0, st, 0, a);
     }
     default: return cudaErrorInvalidValue;
   }

@@ -36,6 +36,8 @@ __global__ void __launch_bounds__(256) k_sb_update(const SbArgs a) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const bool do_tv = a.lam != 0.f, do_w = a.gam != 0.f;
   const float tl = do_tv ? 1.f / a.lam : 0.f, tg = do_w ? 1.f / a.gam : 0.f;
+  pdl_trigger();
+  pdl_wait();
 
   for (int e = tid; e < (TH + 2) * (TW + 2); e += nt) {
     const int u = e / (TW + 2), v = e % (TW + 2);
@@ -46,11 +48,21 @@ __global__ void __launch_bounds__(256) k_sb_update(const SbArgs a) {
 
   if (do_tv) {
     // v_x at rows i0..i0+TH (TH+1), cols j0..j0+TW-1 ; v_y at rows i0..i0+TH-1, cols j0..j0+TW
+    // stage the old b_x / b_y tiles (+1 halo) in shared memory first: loads only
+    for (int e = tid; e < (TH + 1) * TW; e += nt) {
+      const int u = e / TW, v = e % TW;
+      vx[u][v] = a.bx_in[boff + (size_t)((i0 + u) % M) * N + j0 + v];
+    }
+    for (int e = tid; e < TH * (TW + 1); e += nt) {
+      const int u = e / (TW + 1), v = e % (TW + 1);
+      vy[u][v] = a.by_in[boff + (size_t)(i0 + u) * N + (j0 + v) % N];
+    }
+    __syncthreads();
     for (int e = tid; e < (TH + 1) * TW; e += nt) {
       const int u = e / TW, v = e % TW;
       const int gi = (i0 + u) % M, gj = j0 + v;
       const float2 xc = xs[u + 1][v + 1], xm = xs[u][v + 1];
-      const float2 bo = a.bx_in[boff + (size_t)gi * N + gj];
+      const float2 bo = vx[u][v];
       const float2 z = make_float2(xc.x - xm.x + bo.x, xc.y - xm.y + bo.y);
       const float2 d = shrinkc(z, tl);
       const float2 bn = make_float2(z.x - d.x, z.y - d.y);
@@ -61,7 +73,7 @@ __global__ void __launch_bounds__(256) k_sb_update(const SbArgs a) {
       const int u = e / (TW + 1), v = e % (TW + 1);
       const int gi = i0 + u, gj = (j0 + v) % N;
       const float2 xc = xs[u + 1][v + 1], xm = xs[u + 1][v];
-      const float2 bo = a.by_in[boff + (size_t)gi * N + gj];
+      const float2 bo = vy[u][v];
       const float2 z = make_float2(xc.x - xm.x + bo.x, xc.y - xm.y + bo.y);
       const float2 d = shrinkc(z, tl);
       const float2 bn = make_float2(z.x - d.x, z.y - d.y);
@@ -186,8 +198,7 @@ __global__ void __launch_bounds__(256) k_sb_update(const SbArgs a) {
 cudaError_t launch_sb_update(const SbArgs& a, cudaStream_t st) {
   const int TH = a.M < SBT ? a.M : SBT, TW = a.N < SBT ? a.N : SBT;
   if (a.M % TH || a.N % TW || (TH % (1 << a.levels)) || (TW % (1 << a.levels))) return cudaErrorInvalidValue;
-  k_sb_update<<<dim3(a.M / TH, a.N / TW, a.B), 256, 0, st>>>(a);
-  return cudaGetLastError();
+  return launch_ex(k_sb_update, dim3(a.M / TH, a.N / TW, a.B), dim3(256), 0, st, 0, a);
 }
 
 }  // namespace sbk

@@ -5,6 +5,8 @@
 // used here; the Python binding passes raw pointers and a cudaStream_t.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -16,6 +18,16 @@
 #include "kernels.cuh"
 
 using namespace sbk;
+
+namespace sbk {
+thread_local bool g_use_pdl = true;
+}
+
+static bool env_flag(const char* name, bool dflt) {
+  const char* v = getenv(name);
+  if (!v) return dflt;
+  return v[0] == '1';
+}
 
 struct GraphSlot {
   cudaGraphExec_t exec = nullptr;
@@ -403,6 +415,11 @@ static sb_status build_graph(sb_ctx* c, int kind, const sb_pcg_opts* o, const fl
   int64_t l0 = c->launches;
   bool saved_timing = c->timing;
   c->timing = false;
+  struct PdlGuard {
+    bool old;
+    PdlGuard(bool v) : old(g_use_pdl) { g_use_pdl = v; }
+    ~PdlGuard() { g_use_pdl = old; }
+  } pdl_guard(env_flag("SBPCG_GRAPH_PDL", false));
   CK(cudaStreamBeginCaptureToGraph(cs, G, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   sb_status s = SB_OK;
   if (kind == 0) {
@@ -471,6 +488,7 @@ static sb_status build_graph(sb_ctx* c, int kind, const sb_pcg_opts* o, const fl
 // eager (non-graph) execution of one solve whose prelude kind is given
 static sb_status eager_solve(sb_ctx* c, int kind, const sb_pcg_opts* o, const float2* ydev) {
   Loop L = make_loop(c, 0ull);
+  g_use_pdl = env_flag("SBPCG_EAGER_PDL", true);
   sb_status s;
   cudaStream_t st = c->st;
   if (kind == 0) s = seq_resid(c, L, c->bvec, false, false, false, o->eps, o->max_iters, st);
@@ -732,7 +750,7 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   c->G = 1;
   const int tiles = c->N / c->W;
   for (int g = 2; g <= 8; g *= 2)
-    if (c->C % g == 0 && c->M % g == 0 && (int64_t)c->B * tiles * g <= 2 * 148) c->G = g;
+    if (g <= c->C && c->M % g == 0 && (int64_t)c->B * tiles * g <= 2 * 148) c->G = g;
   sb_status s = make_tmap(c);
   if (s) {
     sb_pcg_destroy(c);
