@@ -35,6 +35,11 @@ struct Ctl {
   int pad;
 };
 
+// Instrumentation not reset per call: problem-launches of K1 (for the roofline bytes).
+struct Counters {
+  unsigned long long k1_problems;
+};
+
 enum { ST_OK = 0, ST_NONFINITE = 6, ST_INDEFINITE = 7 };
 
 // Per-kernel-family partial/counter slots.
@@ -55,6 +60,7 @@ struct Loop {
   float* log_relres;     // [slots][B]
   int B;
   unsigned long long cond;  // cudaGraphConditionalHandle (0 = eager)
+  Counters* cnt;            // nullable
 };
 
 // ------------------------------------------------------------------ reductions

@@ -95,6 +95,8 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
     alpha_prev = s.alpha;
   }
 
+  if (g == 0 && tile == 0 && tid == 0 && a.L.cnt != nullptr) atomicAdd(&a.L.cnt->k1_problems, 1ull);
+
   // ---- prologue: the p tile (+halo) into shared memory.  Loads are issued in batches
   // with no global store in between (the x / p_k stores follow in phase 2), so they overlap.
   // PCG forms p_k = z + beta p_{k-1} (standard PCG) and x += alpha p_{k-1}.

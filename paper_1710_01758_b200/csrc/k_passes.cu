@@ -405,22 +405,23 @@ __global__ void __launch_bounds__(256) k_fixup(const PassArgs a) {
   }
 }
 
-// Recon log row for this solve, then advance the solve index (one thread).
+// Recon log row for this solve (one thread per problem), then advance the solve index.
 __global__ void k_log(const Loop L) {
   pdl_trigger();
   pdl_wait();
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const int slot = L.ctl->solve_idx;
-  for (int b = 0; b < L.B; ++b) {
+  for (int b = threadIdx.x; b < L.B; b += blockDim.x) {
     const Scal& s = L.scal[b];
     if (L.log_iters) L.log_iters[(size_t)slot * L.B + b] = s.iter;
     if (L.log_relres) L.log_relres[(size_t)slot * L.B + b] = (float)(s.nb2 > 0 ? sqrt(s.rr / s.nb2) : 0.0);
   }
-  L.ctl->solve_idx = slot + 1;
+  __syncthreads();
+  if (threadIdx.x == 0) L.ctl->solve_idx = slot + 1;
 }
 
 cudaError_t launch_log(const Loop& L, cudaStream_t st) {
-  return launch_ex(k_log, dim3(1), dim3(32), 0, st, 0, L);
+  const int nt = L.B >= 1024 ? 1024 : ((L.B + 31) / 32) * 32;
+  return launch_ex(k_log, dim3(1), dim3(nt), 0, st, 0, L);
 }
 
 // ------------------------------------------------------------------ dispatch

@@ -67,6 +67,7 @@ struct sb_ctx {
   // PCG bookkeeping
   Scal* scal = nullptr;
   Ctl* ctl = nullptr;
+  Counters* counters = nullptr;
   Partials P{};
   float* hist = nullptr;
   int hist_stride = 0;
@@ -161,6 +162,7 @@ static Loop make_loop(sb_ctx* c, unsigned long long cond) {
   L.log_relres = c->log_relres;
   L.B = c->B;
   L.cond = cond;
+  L.cnt = c->counters;
   return L;
 }
 
@@ -630,7 +632,7 @@ void sb_pcg_destroy(sb_ctx* c) {
   void* bufs[] = {c->sens, c->mask, c->rowmask, c->lam_inv, c->kbuf, c->tw_m, c->tw_n, c->twd_m, c->twd_n,
                   c->x, c->r, c->z, c->q, c->p0, c->p1, c->tmp, c->bvec, c->u, c->u1, c->rhs,
                   c->bx[0], c->bx[1], c->by[0], c->by[1], c->bw, c->tmpc, c->stage_in, c->stage_out,
-                  c->scal, c->ctl, c->P.p0, c->P.p1, c->P.cnt, c->hist, c->log_iters, c->log_relres};
+                  c->scal, c->ctl, c->counters, c->P.p0, c->P.p1, c->P.cnt, c->hist, c->log_iters, c->log_relres};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->cap1) cudaStreamDestroy(c->cap1);
@@ -690,6 +692,7 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   for (auto v : vecs) ok &= dalloc(v, BN) == cudaSuccess;
   ok &= dalloc(&c->tmpc, BCN) == cudaSuccess;
   ok &= dalloc(&c->scal, c->B) == cudaSuccess && dalloc(&c->ctl, 1) == cudaSuccess;
+  ok &= dalloc(&c->counters, 1) == cudaSuccess;
   c->P.cap = 4096;
   ok &= dalloc(&c->P.p0, (size_t)c->B * c->P.cap) == cudaSuccess;
   ok &= dalloc(&c->P.p1, (size_t)c->B * c->P.cap) == cudaSuccess;
@@ -742,7 +745,8 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   for (auto v : vecs)
     if (cudaMemsetAsync(*v, 0, BN * sizeof(float2), c->st) != cudaSuccess) return bail(SB_E_CUDA);
   if (cudaMemsetAsync(c->P.cnt, 0, c->B * sizeof(unsigned int), c->st) ||
-      cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st) || cudaMemsetAsync(c->scal, 0, sizeof(Scal) * c->B, c->st))
+      cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st) || cudaMemsetAsync(c->scal, 0, sizeof(Scal) * c->B, c->st) ||
+      cudaMemsetAsync(c->counters, 0, sizeof(Counters), c->st))
     return bail(SB_E_CUDA);
   // K1 configuration: W columns per tile; G-CTA clusters split the coils when the
   // problem alone would not fill the 148 SMs.
@@ -1020,6 +1024,8 @@ sb_status sb_set_kernel_timing(sb_ctx* c, int32_t enable) {
   c->timing = enable != 0;
   c->t_ms[0] = c->t_ms[1] = 0;
   c->t_n[0] = c->t_n[1] = 0;
+  cudaStreamSynchronize(c->st);
+  if (cudaMemset(c->counters, 0, sizeof(Counters)) != cudaSuccess) return fail(c, SB_E_CUDA, "memset counters");
   return SB_OK;
 }
 
@@ -1028,11 +1034,15 @@ sb_status sb_get_kernel_time(sb_ctx* c, int32_t which, double* ms, int64_t* laun
   if (ms) *ms = c->t_ms[which];
   if (launches) *launches = c->t_n[which];
   if (alg_bytes) {
-    // K1 (PCG mode) algorithmic bytes per launch, per problem:
-    // coil maps 8NC + z, p_old, x read + x, p_new, q written (6 x 8N) + mask (4M)
+    // K1 algorithmic bytes per problem-launch: coil maps 8NC
+    // + z, p_{k-1} (and halo), x read + x, p_k, q written (6 x 8N) + row mask (4M);
+    // averaged over the timed launches using the device count of active problems.
     const double N = (double)c->img;
-    *alg_bytes = which == 0 ? (double)c->B * (8.0 * N * c->C + 6.0 * 8.0 * N + 4.0 * c->M)
-                            : (double)c->B * (4.0 * 8.0 * N + 4.0 * N);
+    const double per = which == 0 ? (8.0 * N * c->C + 6.0 * 8.0 * N + 4.0 * c->M) : (4.0 * 8.0 * N + 4.0 * N);
+    Counters h{};
+    if (cudaMemcpy(&h, c->counters, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return fail(c, SB_E_CUDA, "counters");
+    const double probs = (which == 0 && c->t_n[0] > 0) ? (double)h.k1_problems / (double)c->t_n[0] : (double)c->B;
+    *alg_bytes = per * probs;
   }
   return SB_OK;
 }
