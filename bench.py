@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precond", type=int, default=1)
     ap.add_argument("--no-graph", action="store_true")
@@ -62,7 +62,7 @@ def dist_setup():
 
 def workload(cfg: int, ws: int, rank: int, slices_override: int):
     spec = synth.CONFIGS[cfg]
-    if cfg == 3:
+    if cfg in (3, 4):
         per = slices_override or max(1, spec.batch // ws)
         first = rank * per
     else:
@@ -72,6 +72,9 @@ def workload(cfg: int, ws: int, rank: int, slices_override: int):
 
 
 def make_inputs(cfg, first, per):
+    if cfg == 4:  # readout planes of one 3D volume, shared 2D mask (synth.problem_c4)
+        p = synth.problem_c4(range(first, first + per))
+        return p["phantom"], p["sens"], p["mask"], p["noise"]
     ps = [synth.problem2d(cfg, s) for s in range(first, first + per)]
     phantom = np.stack([p["phantom"] for p in ps])
     sens = np.stack([p["sens"] for p in ps])
@@ -154,10 +157,9 @@ def run_reference(args):
         if rank != 0:
             dist.barrier()
             return
-    from oracle import problems, sb
+    from oracle import sb
     spec, per, first = workload(args.config, 1, 0, args.slices)
-    p = synth.problem2d(args.config, first)
-    y = problems.make_kspace(p["phantom"], p["sens"], p["mask"], p["noise"])
+    p, y = oracle_problem(args.config, first)
     prm = spec.params
 
     def sample():
@@ -192,13 +194,24 @@ def run_reference(args):
         dist.barrier()
 
 
+def oracle_problem(cfg, s):
+    """One problem of the workload for the oracle arm: (inputs, oracle k-space y)."""
+    from oracle import problems
+    if cfg == 4:
+        q = synth.problem_c4([s])
+        p = dict(phantom=q["phantom"][0], sens=q["sens"][0].astype(np.complex128), mask=q["mask"],
+                 noise=q["noise"][0].astype(np.complex128))
+    else:
+        p = synth.problem2d(cfg, s)
+    return p, problems.make_kspace(p["phantom"], p["sens"], p["mask"], p["noise"])
+
+
 def cpu_baseline_sample(cfg, precond):
     """Oracle PCG iterations/s on a bounded sample: the first 2 SB outer iterations of slice 0
     (about 10-30 s of single-threaded numpy work at config 2)."""
-    from oracle import problems, sb
+    from oracle import sb
     spec = synth.CONFIGS[cfg]
-    p = synth.problem2d(cfg, 0)
-    y = problems.make_kspace(p["phantom"], p["sens"], p["mask"], p["noise"])
+    p, y = oracle_problem(cfg, 0)
     prm = spec.params
     n_outer = 2
     t = time.perf_counter()
@@ -210,6 +223,23 @@ def cpu_baseline_sample(cfg, precond):
             "sample": f"{n_outer} SB outer iterations of slice 0 ({it} PCG iterations, {dt:.1f} s), "
                       f"numpy fp64 single thread; sb_recon time extrapolates to "
                       f"{dt / n_outer * prm.n_outer:.1f} s for {prm.n_outer} outer"}
+
+
+def kspace_gpu(ctx, spec, phantom, mask_d, noise, dev):
+    """y = R (F S x + sigma n), sigma = 0.005 max|F S x| (reading A21; A29 for a shared
+    mask), formed on the GPU with the library's own encoder (input synthesis, untimed)."""
+    import torch
+    x_d = torch.from_numpy(phantom).to(torch.complex64).to(dev)
+    yfull = ctx.encode(x_d, full=True)
+    if spec.mask_shared:  # reading A29: one noise level over the whole hybrid (x0, k1, k2) data
+        sigma = 0.005 * yfull.abs().amax()
+        mask_c = mask_d.to(torch.complex64)[None, None]
+    else:
+        sigma = 0.005 * yfull.abs().amax(dim=(1, 2, 3), keepdim=True)
+        mask_c = mask_d.to(torch.complex64).unsqueeze(1)
+    yfull.add_(sigma * torch.from_numpy(noise).to(torch.complex64).to(dev))
+    yfull.mul_(mask_c)
+    return yfull
 
 
 def run_ours(args):
@@ -231,13 +261,7 @@ def run_ours(args):
     sens_d = torch.from_numpy(sens).to(torch.complex64).to(dev)
     mask_d = torch.from_numpy(mask).to(dev)
     ctx = SbPcg(sens_d, mask_d, prm.mu, prm.lam, prm.gamma, prm.wavelet_levels)
-    # k-space y = R (F S x + sigma n), sigma = 0.005 max|F S x| (reading A21), on the GPU
-    x_d = torch.from_numpy(phantom).to(torch.complex64).to(dev)
-    yfull = ctx.encode(x_d, full=True)
-    sigma = 0.005 * yfull.abs().amax(dim=(1, 2, 3), keepdim=True)
-    mask_c = mask_d.to(torch.complex64).unsqueeze(1)
-    y_d = (mask_c * (yfull + sigma * torch.from_numpy(noise).to(torch.complex64).to(dev))).contiguous()
-    del yfull
+    y_d = kspace_gpu(ctx, spec, phantom, mask_d, noise, dev)
     out = torch.empty((per, spec.shape[0], spec.shape[1]), dtype=torch.complex64, device=dev)
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
     use_graph = not args.no_graph
@@ -353,11 +377,12 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "PCG iters/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak" if args.config != 3 else "strong",
+            "higher_is_better": True, "scaling": "weak" if args.config not in (3, 4) else "strong",
             "vs_baseline": None, "dtype": "c64 (fp32 complex; Lambda built in f64)",
             "data": "synthetic (seeded phantoms, coil maps, masks; k-space by sb_encode)",
             "config": {"workload": spec.name, "problems_per_gpu": per, "shape": list(spec.shape),
-                       "coils": spec.coils, "mask": "VD lines R=%d, %d-line centre" % (spec.accel, spec.center),
+                       "coils": spec.coils, "mask": ("VD lines R=%d, %d-line centre" % (spec.accel, spec.center)) if spec.mask_kind == "lines"
+                       else ("shared 2D VD random R=%d, %dx%d centre" % (spec.accel, spec.center, spec.center)),
                        "mu": prm.mu, "lambda": prm.lam, "gamma": prm.gamma, "n_outer": prm.n_outer,
                        "pcg_eps": prm.eps, "pcg_max_iters": prm.max_iters,
                        "precond": "circulant" if args.precond else "none",

@@ -59,8 +59,15 @@ typedef enum {
   SB_E_COMM = 10             /* reserved: coil-sharded communicator errors             */
 } sb_status;
 
-/* Problem geometry.  ndim = 2 (3 reserved).  shape = {d0, d1, 0}.  Supported axis
- * lengths: 4, 8, 16, 32, 48, 64, 96, 128, 192, 256 (radix-2/3, reading A23). */
+/* Problem geometry.
+ *   ndim = 2: images [d0][d1], shape = {d0, d1, 0}; d0, d1 in {8, 16, 32, 64, 128, 256}.
+ *             Line masks (constant along d1) take the 1D-FFT matvec (K1); other masks the
+ *             plane-cluster matvec (K1P) for the plane sizes k_plane.cu instantiates.
+ *   ndim = 3: volumes [d0][d1][d2], shape = {d0, d1, d2}; d0 (the readout) in
+ *             {8, ..., 256, 192}, (d1, d2) in {16^2, 32^2, 48^2, 64^2, 128^2, 192^2, 256^2}
+ *             (radix-2/3, reading A23).  The mask must be constant along d0 (fully sampled
+ *             readout; BASELINE config 5), else SB_E_UNSUPPORTED_SIZE.
+ *             wavelet_levels <= 3 (8^3 Haar tiles); TV and Haar are 3D (readings A6, A10). */
 typedef struct {
   int32_t ndim;
   int64_t shape[3];
@@ -154,6 +161,11 @@ sb_status sb_recon(sb_ctx* ctx, const sb_c64* y, const sb_recon_opts* opts, sb_c
  * In-place on b_* is allowed (the only aliasing allowed by the ABI). */
 sb_status sb_sb_update(sb_ctx* ctx, const sb_c64* x, sb_c64* bx, sb_c64* by, sb_c64* bw,
                        sb_c64* rhs_reg);
+
+/* 3D form of sb_sb_update (ndim = 3 contexts; b_z is the third TV auxiliary, 3D Mallat Haar
+ * layout for b_w).  For ndim = 2 contexts bz is ignored and the call equals sb_sb_update. */
+sb_status sb_sb_update3(sb_ctx* ctx, const sb_c64* x, sb_c64* bx, sb_c64* by, sb_c64* bz, sb_c64* bw,
+                        sb_c64* rhs_reg);
 
 /* Real k (not 1/(N k)) as built, fp64 [B or 1][d0][d1] — parity output. */
 sb_status sb_pcg_get_k(sb_ctx* ctx, double* k_out);

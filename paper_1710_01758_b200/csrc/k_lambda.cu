@@ -36,7 +36,8 @@ struct LCol {
 template <int N>
 struct LRow {
   static constexpr int N1 = Split<N>::N1, N2 = Split<N>::N2;
-  static constexpr int LINES = (128 / N2) > 0 ? (128 / N2) : 1;
+  static constexpr int L0 = (128 / N2) > 0 ? (128 / N2) : 1;
+  static constexpr int LINES = (L0 * N1 * (N2 + 1) * 16 > 45000) ? L0 / 2 : L0;  // static smem <= 48 KB
   static constexpr int NT = LINES * N2;
   using Lay = typename RowLayout<N, LINES>::L;
   static constexpr int XS = RowLayout<N, LINES>::size;
@@ -90,6 +91,12 @@ __global__ void __launch_bounds__(LCol<M>::NT) k_lcol(const LamArgs a) {
     for (int q = 0; q < N1; ++q) v[q] = t[(size_t)specidx<M>(j, q) * N + col];
     fft_inv<M, typename C::Lay>(v, xch, tw, j, l);
     const double invN = 1.0 / (double)img;
+    if (a.d3) {  // 3D: the plane k_c only; k / Lambda^{-1} are expanded by k_lexpand3
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1)
+        a.kc2[(size_t)b * img + (size_t)natidx<M>(j, n1) * N + col] = v[n1].x * invN;
+      return;
+    }
     const double PI = 3.14159265358979323846;
     const double sc = sin(PI * (double)col / (double)N);
 #pragma unroll
@@ -140,7 +147,11 @@ __global__ void __launch_bounds__(LRow<N>::NT) k_lrow(const LamArgs a) {
     if (in_range) {
       double2* g = a.g + (size_t)b * img + (size_t)row * N;
 #pragma unroll
-      for (int s = 0; s < N1; ++s) g[specidx<N>(j, s)] = make_double2(acc[s] * inv, 0.0);
+      for (int s = 0; s < N1; ++s) {
+        const int k = specidx<N>(j, s);
+        const double prev = a.accumulate ? g[k].x : 0.0;
+        g[k] = make_double2(prev + acc[s] * inv, 0.0);
+      }
     }
   } else if constexpr (KIND == L_ROW_G || KIND == L_ROW_MASK) {
     double2* t = (KIND == L_ROW_G ? a.g : a.rhat) + (size_t)blockIdx.y * img + (size_t)row * N;
@@ -183,6 +194,23 @@ static cudaError_t lrow(const LamArgs& a, int nimg, cudaStream_t st) {
 }
 
 template <int M, int N>
+static cudaError_t chunk_mn(const LamArgs& a, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = lcol<M, L_COL_SENS>(a, a.B * a.C, st))) return e;
+  return lrow<N, L_ROW_ACC>(a, a.B, st);
+}
+template <int M, int N>
+static cudaError_t tail_mn(const LamArgs& a, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = lcol<M, L_COL_G>(a, a.B, st))) return e;
+  if ((e = lrow<N, L_ROW_G>(a, a.B, st))) return e;
+  if ((e = lcol<M, L_COL_MASK>(a, a.nmask, st))) return e;
+  if ((e = lrow<N, L_ROW_MASK>(a, a.nmask, st))) return e;
+  if ((e = lrow<N, L_ROW_PROD>(a, a.B, st))) return e;
+  return lcol<M, L_COL_FINAL>(a, a.B, st);
+}
+
+template <int M, int N>
 static cudaError_t build_mn(const LamArgs& a, cudaStream_t st) {
   cudaError_t e;
   if ((e = lcol<M, L_COL_SENS>(a, a.B * a.C, st))) return e;
@@ -195,29 +223,53 @@ static cudaError_t build_mn(const LamArgs& a, cudaStream_t st) {
   return lcol<M, L_COL_FINAL>(a, a.B, st);
 }
 
-template <int M>
-static cudaError_t build_m(const LamArgs& a, cudaStream_t st) {
-  switch (a.N) {
-    case 8: return build_mn<M, 8>(a, st);
-    case 16: return build_mn<M, 16>(a, st);
-    case 32: return build_mn<M, 32>(a, st);
-    case 64: return build_mn<M, 64>(a, st);
-    case 128: return build_mn<M, 128>(a, st);
-    case 256: return build_mn<M, 256>(a, st);
-    default: return cudaErrorInvalidValue;
-  }
+#define SBK_LAM_SIZES(X) X(8) X(16) X(32) X(48) X(64) X(128) X(192) X(256)
+
+template <int M, int WHICH>
+static cudaError_t lam_n(const LamArgs& a, cudaStream_t st) {
+#define X(n_) \
+  if (a.N == n_) return WHICH == 0 ? build_mn<M, n_>(a, st) : (WHICH == 1 ? chunk_mn<M, n_>(a, st) : tail_mn<M, n_>(a, st));
+  SBK_LAM_SIZES(X)
+#undef X
+  return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_lambda_build(const LamArgs& a, cudaStream_t st) {
-  switch (a.M) {
-    case 8: return build_m<8>(a, st);
-    case 16: return build_m<16>(a, st);
-    case 32: return build_m<32>(a, st);
-    case 64: return build_m<64>(a, st);
-    case 128: return build_m<128>(a, st);
-    case 256: return build_m<256>(a, st);
-    default: return cudaErrorInvalidValue;
-  }
+template <int WHICH>
+static cudaError_t lam_mn(const LamArgs& a, cudaStream_t st) {
+#define X(m_) \
+  if (a.M == m_) return lam_n<m_, WHICH>(a, st);
+  SBK_LAM_SIZES(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_lambda_build(const LamArgs& a, cudaStream_t st) { return lam_mn<0>(a, st); }
+cudaError_t launch_lambda_chunk(const LamArgs& a, cudaStream_t st) { return lam_mn<1>(a, st); }
+cudaError_t launch_lambda_tail(const LamArgs& a, cudaStream_t st) { return lam_mn<2>(a, st); }
+
+__global__ void __launch_bounds__(256) k_lexpand3(const Lam3Args a) {
+  const size_t pn = (size_t)a.D1 * a.D2, img = pn * a.D0;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (i >= img) return;
+  const int x = (int)(i / pn);
+  const size_t yz = i % pn;
+  const int y = (int)(yz / a.D2), z = (int)(yz % a.D2);
+  const double PI = 3.14159265358979323846;
+  const double s0 = sin(PI * x / (double)a.D0), s1 = sin(PI * y / (double)a.D1), s2 = sin(PI * z / (double)a.D2);
+  const double kd = 4.0 * (s0 * s0 + s1 * s1 + s2 * s2);
+  const double kc = a.kc2[(size_t)b * pn + yz] / (double)a.D0;
+  const double k = a.mu * kc + a.lam * kd + a.gam;
+  const size_t gi = (size_t)b * img + i;
+  a.k_out[gi] = k;
+  if (!(fabs(k) > 1e-14) || !isfinite(k)) atomicExch(a.bad, 1);
+  a.lam_inv[gi] = (float)(1.0 / ((double)img * k));
+}
+
+cudaError_t launch_lambda_expand3(const Lam3Args& a, cudaStream_t st) {
+  const size_t img = (size_t)a.D0 * a.D1 * a.D2;
+  k_lexpand3<<<dim3((unsigned)((img + 255) / 256), a.B), 256, 0, st>>>(a);
+  return cudaGetLastError();
 }
 
 }  // namespace sbk

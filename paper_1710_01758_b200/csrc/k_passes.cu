@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(ColCfg<M, W_>::NT) k_col(const PassArgs a) {
 
   // image / problem index
   int b, c = 0;
-  if constexpr (KIND == P_ENC_COL || KIND == P_GEN_A_COL) {
+  if constexpr (KIND == P_ENC_COL || KIND == P_GEN_A_COL || KIND == P_COL_FWD || KIND == P_COL_INV) {
     b = blockIdx.y / a.C;
     c = blockIdx.y % a.C;
   } else {
@@ -178,6 +178,23 @@ __global__ void __launch_bounds__(ColCfg<M, W_>::NT) k_col(const PassArgs a) {
     float2* t = a.tmp + ((size_t)b * a.C + c) * img;
 #pragma unroll
     for (int s = 0; s < N1; ++s) t[(size_t)specidx<M>(j, s) * N + col] = v[s];
+  } else if constexpr (KIND == P_COL_FWD || KIND == P_COL_INV) {
+    const size_t ioff = ((size_t)b * a.C + c) * img;
+    if constexpr (KIND == P_COL_FWD) {
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) v[n1] = a.a0[ioff + (size_t)natidx<M>(j, n1) * N + col];
+      fft_fwd<M, typename C::Lay>(v, xch, tw, j, l);
+#pragma unroll
+      for (int s = 0; s < N1; ++s)
+        a.o0[ioff + (size_t)specidx<M>(j, s) * N + col] = make_float2(v[s].x * a.scale, v[s].y * a.scale);
+    } else {
+#pragma unroll
+      for (int s = 0; s < N1; ++s) v[s] = a.a0[ioff + (size_t)specidx<M>(j, s) * N + col];
+      fft_inv<M, typename C::Lay>(v, xch, tw, j, l);
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1)
+        a.o0[ioff + (size_t)natidx<M>(j, n1) * N + col] = make_float2(v[n1].x * a.scale, v[n1].y * a.scale);
+    }
   } else if constexpr (KIND == P_ADJ_COL) {
     float2 acc[N1];
     float rss[N1];
@@ -430,7 +447,7 @@ constexpr int kFill = 2 * 148;
 
 template <int M, int KIND>
 static cudaError_t launch_col_t(const PassArgs& a, cudaStream_t st) {
-  const int nimg = (KIND == P_ENC_COL || KIND == P_GEN_A_COL) ? a.B * a.C : a.B;
+  const int nimg = (KIND == P_ENC_COL || KIND == P_GEN_A_COL || KIND == P_COL_FWD || KIND == P_COL_INV) ? a.B * a.C : a.B;
   constexpr int WS = (32 / Split<M>::N2) > 2 ? 32 / Split<M>::N2 : 2;  // >= one warp per CTA
   if (WS < 8 && (a.N / 8) * nimg < kFill) {
     return launch_ex(k_col<M, (WS < 8 ? WS : 8), KIND>, dim3(a.N / WS, nimg), dim3(ColCfg<M, (WS < 8 ? WS : 8)>::NT),
@@ -459,6 +476,7 @@ static cudaError_t col_dispatch(const PassArgs& a, cudaStream_t st) {
     case 32: return launch_col_t<32, KIND>(a, st);
     case 64: return launch_col_t<64, KIND>(a, st);
     case 128: return launch_col_t<128, KIND>(a, st);
+    case 192: return launch_col_t<192, KIND>(a, st);
     case 256: return launch_col_t<256, KIND>(a, st);
     default: return cudaErrorInvalidValue;
   }
@@ -493,6 +511,8 @@ cudaError_t launch_pass(int kind, const PassArgs& a, cudaStream_t st) {
     case P_ADJ_COL: return col_dispatch<P_ADJ_COL>(a, st);
     case P_GEN_A_COL: return col_dispatch<P_GEN_A_COL>(a, st);
     case P_GEN_B_ROW: return row_dispatch<P_GEN_B_ROW>(a, st);
+    case P_COL_FWD: return col_dispatch<P_COL_FWD>(a, st);
+    case P_COL_INV: return col_dispatch<P_COL_INV>(a, st);
     case P_NOPRE: {
       int nb = (int)((img + 2047) / 2048);
       if (nb > 64) nb = 64;

@@ -84,6 +84,22 @@ struct LamArgs {
   const double2* tw_m;
   const double2* tw_n;
   int* bad;                // singular-k flag
+  // 3D (readout-constant mask): the planes of every coil are fed
+  // as extra "coils" of a 2D build in chunks; g accumulates over chunks.
+  int accumulate;          // L_ROW_ACC: g += instead of g =
+  int d3;                  // final pass writes k_c (2D, fp64) to kc2 instead of k / Lambda^{-1}
+  double* kc2;             // [B][D1*D2]
+};
+
+// 3D Lambda: k[x][y][z] = mu kc2[y][z] / D0 + lambda sum_d 4 sin^2(pi nu_d/n_d) + gamma,
+// Lambda^{-1} = 1/(N k)
+struct Lam3Args {
+  int B, D0, D1, D2;
+  double mu, lam, gam;
+  const double* kc2;
+  double* k_out;
+  float* lam_inv;
+  int* bad;
 };
 
 struct SbArgs {
@@ -97,6 +113,46 @@ struct SbArgs {
   float2* bw;              // in place (block-local)
   float2* rhs;             // rhs_reg out
   const Scal* scal;        // nullable
+  // 3D (k_sb_update3): image [B][M][N][D2]
+  int D2;
+  const float2* bz_in;
+  float2* bz_out;
+};
+
+// Plane kernels (k_plane*.cu): one G-CTA cluster per NY x NZ plane, DSMEM-exchanged 2D FFT.
+enum KPMode { KP_APPLY = 0, KP_PCG = 1, KP_RESID = 2, KP_PRECOND = 3, KP_ENCODE = 4, KP_ADJOINT = 5 };
+struct KPArgs {
+  int B, C, planes, NY, NZ;  // image = planes x NY x NZ per problem (2D: planes = 1)
+  int d3;                    // 1: 3D problem (7-point Laplacian across planes)
+  float mu, lam, gam;
+  const float2* sens;        // [B][C][planes][NY][NZ]
+  const uint8_t* mask;       // [B or 1][NY][NZ] (plane mask; 3D masks are constant along d0)
+  int mask_bstride;          // NY*NZ or 0
+  const float* lam_inv;      // PRECOND: [B][planes][NY][NZ]
+  const float2* tw_y;        // [NY]
+  const float2* tw_z;        // [NZ]
+  float scale;               // matvec: 1/(NY NZ); ENCODE/ADJOINT: 1/sqrt(N)
+  int full;                  // ENCODE: R = I
+  const float2* vin;         // APPLY/RESID: p or x ; ENCODE: x
+  float2* out;               // q / r0 / encoded [B][C][img] / adjoint image
+  float2* out2;              // ADJOINT: RSS image (nullable)
+  float2* tmp;               // PRECOND in/out [B][img] ; ADJOINT input [B][C][img]
+  // PCG
+  const float2* z;
+  float2* pbuf0;
+  float2* pbuf1;
+  float2* x;
+  // RESID
+  const float2* bvec;
+  float2* u;
+  const float2* u1;
+  const float2* rhs_reg;
+  float2* bout;
+  int update_u;
+  float eps;
+  int maxit;
+  Loop L;
+  Partials P;
 };
 
 // Programmatic dependent launch on/off for subsequent launches (host-side switch; the
@@ -149,12 +205,23 @@ enum PassKind {
   P_GEN_B_ROW = 8,       // generic matvec: row FFT, x mask/N, row IFFT
   P_NOPRE = 9,           // no preconditioner: r -= alpha q ; z = r ; partials
   P_FIXUP = 10,          // x += alpha p (pending) / x = 0
+  P_COL_FWD = 11,        // o0[b][c] = colFFT(a0[b][c]) * scale   (3D: the d0 transform of E)
+  P_COL_INV = 12,        // o0[b][c] = colIFFT(a0[b][c]) * scale  (3D: the d0 transform of E^H)
 };
 cudaError_t launch_pass(int kind, const PassArgs& a, cudaStream_t st);
 bool pass_supported(int M, int N);
 
+cudaError_t launch_kp2(int mode, const KPArgs& a, cudaStream_t st);  // 2D, matvec modes
+cudaError_t launch_kp3(int mode, const KPArgs& a, cudaStream_t st);  // 3D planes, all modes
+bool kp2_supported(int NY, int NZ);
+bool kp3_supported(int NY, int NZ);
+
 cudaError_t launch_lambda_build(const LamArgs& a, cudaStream_t st);
+cudaError_t launch_lambda_chunk(const LamArgs& a, cudaStream_t st);  // L_COL_SENS + L_ROW_ACC only
+cudaError_t launch_lambda_tail(const LamArgs& a, cudaStream_t st);   // from g to k (or kc2)
+cudaError_t launch_lambda_expand3(const Lam3Args& a, cudaStream_t st);
 cudaError_t launch_sb_update(const SbArgs& a, cudaStream_t st);
+cudaError_t launch_sb_update3(const SbArgs& a, cudaStream_t st);
 cudaError_t launch_log(const Loop& L, cudaStream_t st);
 
 }  // namespace sbk

@@ -45,6 +45,15 @@ struct sb_ctx {
   cudaStream_t cap1 = nullptr;  // graph capture stream (the user stream may be the legacy NULL stream)
   cudaStream_t cap2 = nullptr;  // body capture stream
   int B = 0, C = 0, M = 0, N = 0, L = 0, mask_shared = 0;
+  // geometry: 2D images are D0 x D1 (M = D0, N = D1); 3D volumes D0 x D1 x D2 with
+  // M = D0 (the readout, column-pass length) and N = D1*D2 (column-pass columns)
+  int ndim = 2, D0 = 0, D1 = 0, D2 = 1;
+  bool plane = false;           // K1P plane kernels (2D non-separable masks, or 3D)
+  uint8_t* pmask = nullptr;     // 3D: the plane mask [Bm][D1*D2] (mask constant along d0)
+  float2 *tw_y = nullptr, *tw_z = nullptr;  // plane twiddles (3D: D1, D2)
+  double2 *twd_y = nullptr, *twd_z = nullptr;
+  float2* bz[2] = {nullptr, nullptr};       // 3D TV auxiliary b_z
+  double k1_bytes = 0;          // algorithmic bytes per problem-launch of the matvec
   float mu = 0, lam = 0, gam = 0;
   bool separable = false;
   int W = 8, G = 1;
@@ -120,6 +129,7 @@ static cudaError_t dalloc(T** p, size_t n) {
 }
 
 static bool fft_len_ok(int64_t n) { return n == 8 || n == 16 || n == 32 || n == 64 || n == 128 || n == 256; }
+static bool col3_len_ok(int64_t n) { return fft_len_ok(n) || n == 192; }
 
 // ------------------------------------------------------------------ twiddles
 template <typename V>
@@ -184,6 +194,33 @@ static K1Args base_k1(sb_ctx* c) {
   return a;
 }
 
+static KPArgs base_kp(sb_ctx* c) {
+  KPArgs a;
+  memset(&a, 0, sizeof(a));
+  a.B = c->B;
+  a.C = c->C;
+  a.planes = c->ndim == 3 ? c->D0 : 1;
+  a.NY = c->ndim == 3 ? c->D1 : c->M;
+  a.NZ = c->ndim == 3 ? c->D2 : c->N;
+  a.d3 = c->ndim == 3;
+  a.mu = c->mu;
+  a.lam = c->lam;
+  a.gam = c->gam;
+  a.sens = c->sens;
+  a.mask = c->ndim == 3 ? c->pmask : c->mask;
+  a.mask_bstride = c->mask_shared ? 0 : a.NY * a.NZ;
+  a.lam_inv = c->lam_inv;
+  a.tw_y = c->ndim == 3 ? c->tw_y : c->tw_m;
+  a.tw_z = c->ndim == 3 ? c->tw_z : c->tw_n;
+  a.scale = 1.0f / (float)(a.NY * a.NZ);
+  a.P = c->P;
+  a.pbuf0 = c->p0;
+  a.pbuf1 = c->p1;
+  a.x = c->x;
+  a.z = c->z;
+  return a;
+}
+
 static PassArgs base_pass(sb_ctx* c) {
   PassArgs a;
   memset(&a, 0, sizeof(a));
@@ -235,6 +272,23 @@ static sb_status run_k1(sb_ctx* c, int mode, const K1Args& a, cudaStream_t st) {
   return SB_OK;
 }
 
+static sb_status run_kp(sb_ctx* c, int mode, const KPArgs& a, cudaStream_t st) {
+  const bool timed = c->timing && (mode == KP_APPLY || mode == KP_PCG || mode == KP_RESID);
+  int e0 = -1;
+  if (timed) {
+    e0 = (int)c->evnext;
+    CK(cudaEventRecord(ev_get(c), st));
+  }
+  CK(c->ndim == 3 ? launch_kp3(mode, a, st) : launch_kp2(mode, a, st));
+  if (timed) {
+    int e1 = (int)c->evnext;
+    CK(cudaEventRecord(ev_get(c), st));
+    c->evpend.push_back({0, {e0, e1}});
+  }
+  c->launches++;
+  return SB_OK;
+}
+
 static sb_status run_pass(sb_ctx* c, int kind, const PassArgs& a, cudaStream_t st) {
   CK(launch_pass(kind, a, st));
   c->launches++;
@@ -257,6 +311,12 @@ static void timing_collect(sb_ctx* c) {
 // ------------------------------------------------------------------ kernel sequences
 // q = A v (generic or separable)
 static sb_status seq_apply(sb_ctx* c, const float2* v, float2* out, cudaStream_t st) {
+  if (c->plane) {
+    KPArgs k = base_kp(c);
+    k.vin = v;
+    k.out = out;
+    return run_kp(c, KP_APPLY, k, st);
+  }
   if (!c->separable) {
     PassArgs pa = base_pass(c);
     pa.a0 = v;
@@ -276,6 +336,21 @@ static sb_status seq_apply(sb_ctx* c, const float2* v, float2* out, cudaStream_t
 // r0 = b - A x (+ recon RHS/feedback), fin_init
 static sb_status seq_resid(sb_ctx* c, Loop L, const float2* bgiven, bool recon, bool update_u, bool use_rhs,
                            float eps, int maxit, cudaStream_t st) {
+  if (c->plane) {
+    KPArgs k = base_kp(c);
+    k.vin = c->x;
+    k.out = c->r;
+    k.bvec = recon ? nullptr : bgiven;
+    k.u = c->u;
+    k.u1 = c->u1;
+    k.rhs_reg = use_rhs ? c->rhs : nullptr;
+    k.bout = c->bvec;
+    k.update_u = update_u ? 1 : 0;
+    k.eps = eps;
+    k.maxit = maxit;
+    k.L = L;
+    return run_kp(c, KP_RESID, k, st);
+  }
   if (!c->separable) {
     PassArgs pa = base_pass(c);
     pa.a0 = c->x;
@@ -321,7 +396,14 @@ static sb_status seq_precond(sb_ctx* c, Loop L, int precond, int mode, const flo
   pa.o0 = c->r;
   pa.tmp = c->tmp;
   if ((s = run_pass(c, P_PRE_A_FWD_COL, pa, st))) return s;
-  if ((s = run_pass(c, P_PRE_B_ROW, pa, st))) return s;
+  if (c->ndim == 3) {  // d0 FFT (pass A) -> plane FFT x Lambda^{-1} x plane IFFT -> d0 IFFT (pass C)
+    KPArgs k = base_kp(c);
+    k.tmp = c->tmp;
+    k.L = L;
+    if ((s = run_kp(c, KP_PRECOND, k, st))) return s;
+  } else if ((s = run_pass(c, P_PRE_B_ROW, pa, st))) {
+    return s;
+  }
   pa.a0 = (mode >= 0) ? c->r : nullptr;
   pa.o0 = zout;
   return run_pass(c, P_PRE_C_INV_COL, pa, st);
@@ -330,6 +412,15 @@ static sb_status seq_precond(sb_ctx* c, Loop L, int precond, int mode, const flo
 static sb_status seq_body(sb_ctx* c, Loop L, int precond, cudaStream_t st, int* nk) {
   int n0 = (int)c->launches;
   sb_status s;
+  if (c->plane) {
+    KPArgs k = base_kp(c);
+    k.out = c->q;
+    k.L = L;
+    if ((s = run_kp(c, KP_PCG, k, st))) return s;
+    if ((s = seq_precond(c, L, precond, 1, c->r, c->z, st))) return s;
+    if (nk) *nk = (int)c->launches - n0;
+    return SB_OK;
+  }
   if (!c->separable) {
     PassArgs pa = base_pass(c);
     pa.L = L;
@@ -378,12 +469,45 @@ static sb_status seq_shrink(sb_ctx* c, int par, cudaStream_t st) {
   a.by_out = c->by[1 - par];
   a.bw = c->bw;
   a.rhs = c->rhs;
+  if (c->ndim == 3) {
+    a.M = c->D0;
+    a.N = c->D1;
+    a.D2 = c->D2;
+    a.bz_in = c->bz[par];
+    a.bz_out = c->bz[1 - par];
+    CK(launch_sb_update3(a, st));
+    c->launches++;
+    return SB_OK;
+  }
   CK(launch_sb_update(a, st));
   c->launches++;
   return SB_OK;
 }
 
+// 3D adjoint: d0 IFFT of every coil's k-space (column pass), then per plane the masked plane
+// IFFT, conj(s_c) combine and (optionally) the root sum of squares (K1P adjoint mode).
+static sb_status seq_adjoint3(sb_ctx* c, const float2* ydev, float2* xout, float2* rssout, cudaStream_t st) {
+  PassArgs pa = base_pass(c);
+  pa.a0 = ydev;
+  pa.o0 = c->tmpc;
+  pa.scale = 1.0f;
+  sb_status s;
+  if ((s = run_pass(c, P_COL_INV, pa, st))) return s;
+  KPArgs k = base_kp(c);
+  k.tmp = c->tmpc;
+  k.out = xout;
+  k.out2 = rssout;
+  k.scale = 1.0f / std::sqrt((float)c->img);
+  return run_kp(c, KP_ADJOINT, k, st);
+}
+
 static sb_status seq_init_recon(sb_ctx* c, const float2* ydev, cudaStream_t st) {
+  if (c->ndim == 3) {
+    sb_status s = seq_adjoint3(c, ydev, c->u1, c->x, st);
+    if (s) return s;
+    CK(cudaMemcpyAsync(c->u, c->u1, c->img * c->B * sizeof(float2), cudaMemcpyDeviceToDevice, st));
+    return SB_OK;
+  }
   PassArgs pa = base_pass(c);
   pa.a0 = ydev;
   pa.tmp = c->tmpc;
@@ -525,7 +649,11 @@ static sb_status run_solve_kind(sb_ctx* c, int kind, const sb_pcg_opts* o, const
 }
 
 // ------------------------------------------------------------------ Lambda build
+static sb_status build_lambda3(sb_ctx* c);
+static sb_status finish_lambda(sb_ctx* c, void* tmp, void* g, void* rh, int* bad, void* kc2);
+
 static sb_status build_lambda(sb_ctx* c) {
+  if (c->ndim == 3) return build_lambda3(c);
   LamArgs a;
   memset(&a, 0, sizeof(a));
   a.B = c->B;
@@ -557,6 +685,78 @@ static sb_status build_lambda(sb_ctx* c) {
   a.bad = bad;
   CK(launch_lambda_build(a, c->st));
   c->launches += 8;
+  return finish_lambda(c, tmp, g, rh, bad, nullptr);
+}
+
+// 3D (mask constant along d0): with F_3 = F_0 (x) F_12 and Parseval along d0,
+//   sum_{q0} g(q0, q) = D0 sum_c sum_x |D_12 s_c(x)|^2 (q) / N^2,
+// and k_c is constant along nu_0 and equals the 2D correlation of that marginal with the
+// plane mask.  The planes of every coil are fed to the 2D build
+// as extra "coils" in chunks (g accumulates), then k / Lambda^{-1} are expanded to 3D.
+static sb_status build_lambda3(sb_ctx* c) {
+  const size_t pn = (size_t)c->D1 * c->D2;
+  const int nplanes = c->C * c->D0;  // per problem
+  const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)nplanes, (size_t)(64u << 20) / (pn * 16)));
+  LamArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = c->D1;
+  a.N = c->D2;
+  a.mu = c->mu;
+  a.lam = c->lam;
+  a.gam = c->gam;
+  a.mask_bstride = c->mask_shared ? 0 : (int)pn;
+  a.nmask = c->mask_shared ? 1 : c->B;
+  a.tw_m = c->twd_y;
+  a.tw_n = c->twd_z;
+  double2 *tmp = nullptr, *g = nullptr, *rh = nullptr;
+  double* kc2 = nullptr;
+  int* bad = nullptr;
+  CK(dalloc(&tmp, (size_t)chunk * pn));
+  CK(dalloc(&g, (size_t)c->B * pn));
+  CK(dalloc(&rh, (size_t)a.nmask * pn));
+  CK(dalloc(&kc2, (size_t)c->B * pn));
+  CK(dalloc(&bad, 1));
+  CK(cudaMemsetAsync(bad, 0, sizeof(int), c->st));
+  a.tmp = tmp;
+  a.rhat = rh;
+  a.bad = bad;
+  for (int b = 0; b < c->B; ++b) {
+    for (int p0 = 0; p0 < nplanes; p0 += chunk) {
+      a.B = 1;
+      a.C = std::min(chunk, nplanes - p0);
+      a.sens = c->sens + ((size_t)b * nplanes + p0) * pn;
+      a.g = g + (size_t)b * pn;
+      a.accumulate = p0 > 0;
+      CK(launch_lambda_chunk(a, c->st));
+      c->launches += 2;
+    }
+  }
+  a.B = c->B;
+  a.C = 1;
+  a.g = g;
+  a.mask = c->pmask;
+  a.d3 = 1;
+  a.kc2 = kc2;
+  CK(launch_lambda_tail(a, c->st));
+  c->launches += 6;
+  Lam3Args e;
+  e.B = c->B;
+  e.D0 = c->D0;
+  e.D1 = c->D1;
+  e.D2 = c->D2;
+  e.mu = c->mu;
+  e.lam = c->lam;
+  e.gam = c->gam;
+  e.kc2 = kc2;
+  e.k_out = c->kbuf;
+  e.lam_inv = c->lam_inv;
+  e.bad = bad;
+  CK(launch_lambda_expand3(e, c->st));
+  c->launches += 1;
+  return finish_lambda(c, tmp, g, rh, bad, kc2);
+}
+
+static sb_status finish_lambda(sb_ctx* c, void* tmp, void* g, void* rh, int* bad, void* kc2) {
   int hb = 0;
   CK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
@@ -564,6 +764,7 @@ static sb_status build_lambda(sb_ctx* c) {
   cudaFree(g);
   cudaFree(rh);
   cudaFree(bad);
+  if (kc2) cudaFree(kc2);
   if (hb) return fail(c, SB_E_SINGULAR_K, "singular k (min |k| <= 1e-14 or non-finite)");
   return SB_OK;
 }
@@ -632,7 +833,8 @@ void sb_pcg_destroy(sb_ctx* c) {
   void* bufs[] = {c->sens, c->mask, c->rowmask, c->lam_inv, c->kbuf, c->tw_m, c->tw_n, c->twd_m, c->twd_n,
                   c->x, c->r, c->z, c->q, c->p0, c->p1, c->tmp, c->bvec, c->u, c->u1, c->rhs,
                   c->bx[0], c->bx[1], c->by[0], c->by[1], c->bw, c->tmpc, c->stage_in, c->stage_out,
-                  c->scal, c->ctl, c->counters, c->P.p0, c->P.p1, c->P.cnt, c->hist, c->log_iters, c->log_relres};
+                  c->scal, c->ctl, c->counters, c->P.p0, c->P.p1, c->P.cnt, c->hist, c->log_iters, c->log_relres,
+                  c->pmask, c->tw_y, c->tw_z, c->twd_y, c->twd_z, c->bz[0], c->bz[1]};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->cap1) cudaStreamDestroy(c->cap1);
@@ -645,13 +847,23 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   if (!out) return SB_E_ARG;
   *out = nullptr;
   if (!dims || !mask || !sens) return SB_E_ARG;
-  if (dims->ndim != 2) return SB_E_DIM;
+  if (dims->ndim != 2 && dims->ndim != 3) return SB_E_DIM;
   if (dims->batch < 1 || coils < 1 || dims->wavelet_levels < 0) return SB_E_DIM;
-  const int64_t M = dims->shape[0], N = dims->shape[1];
-  if (!fft_len_ok(M) || !fft_len_ok(N)) return SB_E_UNSUPPORTED_SIZE;
+  const bool d3 = dims->ndim == 3;
+  const int64_t D0 = dims->shape[0], D1 = dims->shape[1], D2 = d3 ? dims->shape[2] : 1;
+  const int64_t M = D0, N = D1 * D2;  // column-pass geometry
   const int Lv = dims->wavelet_levels;
-  const int TH = M < 32 ? (int)M : 32, TW = N < 32 ? (int)N : 32;
-  if (Lv > 5 || (TH % (1 << Lv)) || (TW % (1 << Lv))) return SB_E_DIM;
+  if (!d3) {
+    if (!fft_len_ok(D0) || !fft_len_ok(D1)) return SB_E_UNSUPPORTED_SIZE;
+    const int TH = M < 32 ? (int)M : 32, TW = N < 32 ? (int)N : 32;
+    if (Lv > 5 || (TH % (1 << Lv)) || (TW % (1 << Lv))) return SB_E_DIM;
+  } else {
+    if (!col3_len_ok(D0) || !kp3_supported((int)D1, (int)D2)) return SB_E_UNSUPPORTED_SIZE;
+    for (int64_t d : {D0, D1, D2}) {
+      const int64_t T = d < 8 ? d : 8;
+      if (Lv > 3 || d % T || T % (1 << Lv)) return SB_E_DIM;
+    }
+  }
   if (!(gamma > 0.f) || mu < 0.f || lambda < 0.f || !std::isfinite(mu) || !std::isfinite(lambda) ||
       !std::isfinite(gamma))
     return SB_E_PARAM;
@@ -663,6 +875,10 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   c->C = coils;
   c->M = (int)M;
   c->N = (int)N;
+  c->ndim = dims->ndim;
+  c->D0 = (int)D0;
+  c->D1 = (int)D1;
+  c->D2 = (int)D2;
   c->L = Lv;
   c->mask_shared = dims->mask_shared ? 1 : 0;
   c->mu = mu;
@@ -691,9 +907,15 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
                      &c->bx[0], &c->bx[1], &c->by[0], &c->by[1], &c->bw};
   for (auto v : vecs) ok &= dalloc(v, BN) == cudaSuccess;
   ok &= dalloc(&c->tmpc, BCN) == cudaSuccess;
+  if (d3) {
+    ok &= dalloc(&c->pmask, (c->mask_shared ? 1 : c->B) * (size_t)D1 * D2) == cudaSuccess;
+    ok &= dalloc(&c->bz[0], BN) == cudaSuccess && dalloc(&c->bz[1], BN) == cudaSuccess;
+    ok &= dalloc(&c->tw_y, D1) == cudaSuccess && dalloc(&c->tw_z, D2) == cudaSuccess;
+    ok &= dalloc(&c->twd_y, D1) == cudaSuccess && dalloc(&c->twd_z, D2) == cudaSuccess;
+  }
   ok &= dalloc(&c->scal, c->B) == cudaSuccess && dalloc(&c->ctl, 1) == cudaSuccess;
   ok &= dalloc(&c->counters, 1) == cudaSuccess;
-  c->P.cap = 4096;
+  c->P.cap = (int)std::max<int64_t>(4096, N / 2 + 64);  // column passes: N/W partials, W >= 2
   ok &= dalloc(&c->P.p0, (size_t)c->B * c->P.cap) == cudaSuccess;
   ok &= dalloc(&c->P.p1, (size_t)c->B * c->P.cap) == cudaSuccess;
   ok &= dalloc(&c->P.cnt, c->B) == cudaSuccess;
@@ -707,32 +929,49 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   cudaMemcpyKind km = is_device_ptr(mask) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   if (cudaMemcpyAsync(c->sens, sens, BCN * sizeof(float2), ks, c->st) != cudaSuccess) return bail(SB_E_CUDA);
   if (cudaMemcpyAsync(c->mask, mask, nmask, km, c->st) != cudaSuccess) return bail(SB_E_CUDA);
-  // separability (rows constant along d1) on the host
   std::vector<uint8_t> hm(nmask);
   if (cudaMemcpyAsync(hm.data(), c->mask, nmask, cudaMemcpyDeviceToHost, c->st) != cudaSuccess ||
       cudaStreamSynchronize(c->st) != cudaSuccess)
     return bail(SB_E_CUDA);
-  bool sep = true;
+  for (uint8_t v : hm)
+    if (v > 1) return bail(SB_E_ARG);
   const int nm = c->mask_shared ? 1 : c->B;
-  std::vector<float> rm((size_t)nm * M);
-  for (int b = 0; b < nm && sep; ++b)
-    for (int64_t i = 0; i < M && sep; ++i) {
-      const uint8_t* row = hm.data() + (size_t)b * img + (size_t)i * N;
-      for (int64_t j = 0; j < N; ++j) {
-        if (row[j] > 1) {
-          sb_pcg_destroy(c);
-          return SB_E_ARG;
-        }
-        if (row[j] != row[0]) {
-          sep = false;
-          break;
-        }
+  if (!d3) {
+    // separability (rows constant along d1): the line-mask identity of K1 (DESIGN.md a1)
+    bool sep = true;
+    std::vector<float> rm((size_t)nm * M);
+    for (int b = 0; b < nm && sep; ++b)
+      for (int64_t i = 0; i < M && sep; ++i) {
+        const uint8_t* row = hm.data() + (size_t)b * img + (size_t)i * N;
+        for (int64_t j = 0; j < N; ++j)
+          if (row[j] != row[0]) {
+            sep = false;
+            break;
+          }
+        rm[(size_t)b * M + i] = row[0] ? 1.0f / (float)M : 0.f;
       }
-      rm[(size_t)b * M + i] = row[0] ? 1.0f / (float)M : 0.f;
-    }
-  c->separable = sep;
-  if (sep && cudaMemcpy(c->rowmask, rm.data(), rm.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
-    return bail(SB_E_CUDA);
+    c->separable = sep;
+    c->plane = !sep && kp2_supported((int)M, (int)N);
+    if (sep && cudaMemcpy(c->rowmask, rm.data(), rm.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(SB_E_CUDA);
+  } else {
+    // 3D: the mask must be constant along the readout d0 (BASELINE config 5):
+    // then the data term factors per d0 plane (k_plane.cu)
+    const size_t pn = (size_t)D1 * D2;
+    for (int b = 0; b < nm; ++b)
+      for (int64_t x = 1; x < D0; ++x)
+        if (memcmp(hm.data() + (size_t)b * img + x * pn, hm.data() + (size_t)b * img, pn) != 0) {
+          c->err = "3D mask must be constant along the readout axis d0";
+          sb_pcg_destroy(c);
+          return SB_E_UNSUPPORTED_SIZE;
+        }
+    for (int b = 0; b < nm; ++b)
+      if (cudaMemcpy(c->pmask + (size_t)b * pn, hm.data() + (size_t)b * img, pn, cudaMemcpyHostToDevice) !=
+          cudaSuccess)
+        return bail(SB_E_CUDA);
+    c->separable = false;
+    c->plane = true;
+  }
   // twiddles
   auto tm = make_tw<float2>((int)M), tn = make_tw<float2>((int)N);
   auto tdm = make_tw<double2>((int)M), tdn = make_tw<double2>((int)N);
@@ -741,9 +980,21 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
       cudaMemcpy(c->twd_m, tdm.data(), M * sizeof(double2), cudaMemcpyHostToDevice) ||
       cudaMemcpy(c->twd_n, tdn.data(), N * sizeof(double2), cudaMemcpyHostToDevice))
     return bail(SB_E_CUDA);
+  if (d3) {
+    auto ty = make_tw<float2>((int)D1), tz = make_tw<float2>((int)D2);
+    auto tdy = make_tw<double2>((int)D1), tdz = make_tw<double2>((int)D2);
+    if (cudaMemcpy(c->tw_y, ty.data(), D1 * sizeof(float2), cudaMemcpyHostToDevice) ||
+        cudaMemcpy(c->tw_z, tz.data(), D2 * sizeof(float2), cudaMemcpyHostToDevice) ||
+        cudaMemcpy(c->twd_y, tdy.data(), D1 * sizeof(double2), cudaMemcpyHostToDevice) ||
+        cudaMemcpy(c->twd_z, tdz.data(), D2 * sizeof(double2), cudaMemcpyHostToDevice))
+      return bail(SB_E_CUDA);
+  }
   // zero state
   for (auto v : vecs)
     if (cudaMemsetAsync(*v, 0, BN * sizeof(float2), c->st) != cudaSuccess) return bail(SB_E_CUDA);
+  if (d3 && (cudaMemsetAsync(c->bz[0], 0, BN * sizeof(float2), c->st) ||
+             cudaMemsetAsync(c->bz[1], 0, BN * sizeof(float2), c->st)))
+    return bail(SB_E_CUDA);
   if (cudaMemsetAsync(c->P.cnt, 0, c->B * sizeof(unsigned int), c->st) ||
       cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st) || cudaMemsetAsync(c->scal, 0, sizeof(Scal) * c->B, c->st) ||
       cudaMemsetAsync(c->counters, 0, sizeof(Counters), c->st))
@@ -755,7 +1006,12 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   const int tiles = c->N / c->W;
   for (int g = 2; g <= 8; g *= 2)
     if (g <= c->C && c->M % g == 0 && (int64_t)c->B * tiles * g <= 2 * 148) c->G = g;
-  sb_status s = make_tmap(c);
+  // algorithmic bytes per problem-launch of the matvec: coil maps
+  // 8NC + z, p_{k-1}, x read + p_k, x, q written (6 x 8N) + the mask (4M floats for line
+  // masks, one byte per plane pixel otherwise)
+  c->k1_bytes = 8.0 * (double)img * c->C + 48.0 * (double)img +
+                (c->separable ? 4.0 * c->M : (double)(d3 ? (size_t)D1 * D2 : img));
+  sb_status s = c->separable ? make_tmap(c) : SB_OK;
   if (s) {
     sb_pcg_destroy(c);
     return s;
@@ -821,14 +1077,28 @@ sb_status sb_encode(sb_ctx* c, const sb_c64* x, sb_c64* y, int32_t full) {
   if ((s = stage_in(c, x, bytes, &xd, c->tmp))) return s;
   if (hy && !c->stage_out) CK(dalloc(&c->stage_out, c->B * c->C * c->img));
   float2* yd = hy ? c->stage_out : (float2*)y;
-  PassArgs pa = base_pass(c);
-  pa.a0 = (const float2*)xd;
-  pa.tmp = c->tmpc;
-  pa.o0 = yd;
-  pa.full = full ? 1 : 0;
-  pa.scale = 1.0f / std::sqrt((float)c->img);
-  if ((s = run_pass(c, P_ENC_COL, pa, c->st))) return s;
-  if ((s = run_pass(c, P_ENC_ROW, pa, c->st))) return s;
+  if (c->ndim == 3) {  // per plane: (R) F_12 (s_c x) -> tmpc ; then the d0 FFT of every coil
+    KPArgs k = base_kp(c);
+    k.vin = (const float2*)xd;
+    k.out = c->tmpc;
+    k.full = full ? 1 : 0;
+    k.scale = 1.0f / std::sqrt((float)c->img);
+    if ((s = run_kp(c, KP_ENCODE, k, c->st))) return s;
+    PassArgs pa = base_pass(c);
+    pa.a0 = c->tmpc;
+    pa.o0 = yd;
+    pa.scale = 1.0f;
+    if ((s = run_pass(c, P_COL_FWD, pa, c->st))) return s;
+  } else {
+    PassArgs pa = base_pass(c);
+    pa.a0 = (const float2*)xd;
+    pa.tmp = c->tmpc;
+    pa.o0 = yd;
+    pa.full = full ? 1 : 0;
+    pa.scale = 1.0f / std::sqrt((float)c->img);
+    if ((s = run_pass(c, P_ENC_COL, pa, c->st))) return s;
+    if ((s = run_pass(c, P_ENC_ROW, pa, c->st))) return s;
+  }
   if (hy) {
     CK(cudaMemcpyAsync(y, yd, ybytes, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
@@ -846,14 +1116,18 @@ sb_status sb_adjoint(sb_ctx* c, const sb_c64* y, sb_c64* x) {
   const void* yd;
   if ((s = stage_in(c, y, ybytes, &yd, c->stage_in))) return s;
   float2* xd = hx ? c->q : (float2*)x;
-  PassArgs pa = base_pass(c);
-  pa.a0 = (const float2*)yd;
-  pa.tmp = c->tmpc;
-  pa.o0 = xd;
-  pa.o1 = nullptr;
-  pa.scale = 1.0f / std::sqrt((float)c->img);
-  if ((s = run_pass(c, P_ADJ_ROW, pa, c->st))) return s;
-  if ((s = run_pass(c, P_ADJ_COL, pa, c->st))) return s;
+  if (c->ndim == 3) {
+    if ((s = seq_adjoint3(c, (const float2*)yd, xd, nullptr, c->st))) return s;
+  } else {
+    PassArgs pa = base_pass(c);
+    pa.a0 = (const float2*)yd;
+    pa.tmp = c->tmpc;
+    pa.o0 = xd;
+    pa.o1 = nullptr;
+    pa.scale = 1.0f / std::sqrt((float)c->img);
+    if ((s = run_pass(c, P_ADJ_ROW, pa, c->st))) return s;
+    if ((s = run_pass(c, P_ADJ_COL, pa, c->st))) return s;
+  }
   if (hx) {
     CK(cudaMemcpyAsync(x, xd, bytes, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
@@ -946,8 +1220,9 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
                      c->st));
   const void* yd = c->stage_in;
   // fresh SB state (Alg. 1 step 1)
-  float2* zs[] = {c->bx[0], c->bx[1], c->by[0], c->by[1], c->bw, c->rhs};
-  for (auto v : zs) CK(cudaMemsetAsync(v, 0, bytes, c->st));
+  float2* zs[] = {c->bx[0], c->bx[1], c->by[0], c->by[1], c->bw, c->rhs, c->bz[0], c->bz[1]};
+  for (auto v : zs)
+    if (v) CK(cudaMemsetAsync(v, 0, bytes, c->st));
   CK(cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st));
   if (c->timing) c->evnext = 0;
   const sb_pcg_opts* o = &ro->pcg;
@@ -988,9 +1263,33 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
   return status_from_scal(c);
 }
 
+sb_status sb_sb_update3(sb_ctx* c, const sb_c64* x, sb_c64* bx, sb_c64* by, sb_c64* bz, sb_c64* bw,
+                        sb_c64* rhs_reg) {
+  sb_status s = check_ready(c);
+  if (s) return s;
+  if (!x || !bx || !by || !bw || !rhs_reg || (c->ndim == 3 && !bz)) return fail(c, SB_E_ARG, "sb_update: null pointer");
+  const size_t bytes = c->B * c->img * sizeof(float2);
+  auto kin = [&](const void* p) { return is_device_ptr(p) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice; };
+  auto kout = [&](const void* p) { return is_device_ptr(p) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost; };
+  CK(cudaMemcpyAsync(c->x, x, bytes, kin(x), c->st));
+  CK(cudaMemcpyAsync(c->bx[0], bx, bytes, kin(bx), c->st));
+  CK(cudaMemcpyAsync(c->by[0], by, bytes, kin(by), c->st));
+  if (c->ndim == 3) CK(cudaMemcpyAsync(c->bz[0], bz, bytes, kin(bz), c->st));
+  CK(cudaMemcpyAsync(c->bw, bw, bytes, kin(bw), c->st));
+  if ((s = seq_shrink(c, 0, c->st))) return s;
+  CK(cudaMemcpyAsync(bx, c->bx[1], bytes, kout(bx), c->st));
+  CK(cudaMemcpyAsync(by, c->by[1], bytes, kout(by), c->st));
+  if (c->ndim == 3) CK(cudaMemcpyAsync(bz, c->bz[1], bytes, kout(bz), c->st));
+  CK(cudaMemcpyAsync(bw, c->bw, bytes, kout(bw), c->st));
+  CK(cudaMemcpyAsync(rhs_reg, c->rhs, bytes, kout(rhs_reg), c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return SB_OK;
+}
+
 sb_status sb_sb_update(sb_ctx* c, const sb_c64* x, sb_c64* bx, sb_c64* by, sb_c64* bw, sb_c64* rhs_reg) {
   sb_status s = check_ready(c);
   if (s) return s;
+  if (c->ndim == 3) return fail(c, SB_E_DIM, "sb_sb_update is 2D; use sb_sb_update3");
   if (!x || !bx || !by || !bw || !rhs_reg) return fail(c, SB_E_ARG, "sb_update: null pointer");
   const size_t bytes = c->B * c->img * sizeof(float2);
   auto kin = [&](const void* p) { return is_device_ptr(p) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice; };
@@ -1038,7 +1337,7 @@ sb_status sb_get_kernel_time(sb_ctx* c, int32_t which, double* ms, int64_t* laun
     // + z, p_{k-1} (and halo), x read + x, p_k, q written (6 x 8N) + row mask (4M);
     // averaged over the timed launches using the device count of active problems.
     const double N = (double)c->img;
-    const double per = which == 0 ? (8.0 * N * c->C + 6.0 * 8.0 * N + 4.0 * c->M) : (4.0 * 8.0 * N + 4.0 * N);
+    const double per = which == 0 ? c->k1_bytes : (4.0 * 8.0 * N + 4.0 * N);
     Counters h{};
     if (cudaMemcpy(&h, c->counters, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return fail(c, SB_E_CUDA, "counters");
     const double probs = (which == 0 && c->t_n[0] > 0) ? (double)h.k1_problems / (double)c->t_n[0] : (double)c->B;

@@ -10,6 +10,7 @@ import ctypes as C
 import os
 from typing import Optional
 
+import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -56,6 +57,7 @@ _sig = {
     "sb_pcg_solve": (C.c_int, [_vp, _vp, _vp, C.POINTER(SbPcgOpts), C.POINTER(SbPcgStats)]),
     "sb_recon": (C.c_int, [_vp, _vp, C.POINTER(SbReconOpts), _vp, C.POINTER(SbReconLog)]),
     "sb_sb_update": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "sb_sb_update3": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "sb_pcg_get_k": (C.c_int, [_vp, _vp]),
     "sb_set_kernel_timing": (C.c_int, [_vp, C.c_int32]),
     "sb_get_kernel_time": (C.c_int, [_vp, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64),
@@ -96,18 +98,27 @@ class SbPcg:
 
     def __init__(self, sens: torch.Tensor, mask: torch.Tensor, mu: float, lam: float, gamma: float,
                  levels: int = 1, stream: Optional[torch.cuda.Stream] = None):
+        """sens: complex64 [B,C,M,N] (2D) or [B,C,D0,D1,D2] (3D; a 4D tensor is read as 2D);
+        mask: uint8 [B,*image] or [*image] (shared).  3D masks must be constant along D0."""
+        if sens.dtype != torch.complex64 or mask.dtype != torch.uint8:
+            raise TypeError("sens must be complex64 [B,C,*image], mask uint8 [B,*image] or [*image]")
         if sens.dim() == 3:
             sens = sens.unsqueeze(0)
-        if sens.dtype != torch.complex64 or mask.dtype != torch.uint8:
-            raise TypeError("sens must be complex64 [B,C,M,N], mask uint8 [B,M,N] or [M,N]")
-        B, Cc, M, N = sens.shape
-        shared = mask.dim() == 2 or (mask.dim() == 3 and mask.shape[0] == 1 and B > 1)
-        self.B, self.C, self.M, self.N = B, Cc, M, N
+        nd = sens.dim() - 2
+        if nd not in (2, 3):
+            raise ValueError("sens must be [B,C,M,N] or [B,C,D0,D1,D2]")
+        B, Cc = sens.shape[0], sens.shape[1]
+        self.image = tuple(int(v) for v in sens.shape[2:])
+        shared = mask.dim() == nd or (mask.dim() == nd + 1 and mask.shape[0] == 1 and B > 1)
+        self.ndim = nd
+        self.B, self.C = B, Cc
+        self.M, self.N = self.image[0], int(np.prod(self.image[1:]))
         self.device = sens.device if sens.is_cuda else torch.device("cuda", torch.cuda.current_device())
         self._stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self._sens = sens.contiguous()
         self._mask = mask.contiguous()
-        d = SbDims(2, (C.c_int64 * 3)(M, N, 0), B, levels, 1 if shared else 0)
+        shp = list(self.image) + [0] * (3 - nd)
+        d = SbDims(nd, (C.c_int64 * 3)(*shp), B, levels, 1 if shared else 0)
         h = _vp()
         st = _lib.sb_pcg_create(C.byref(h), C.byref(d), Cc, _ptr(self._mask), _ptr(self._sens),
                                 float(mu), float(lam), float(gamma), _vp(self._stream.cuda_stream))
@@ -133,7 +144,7 @@ class SbPcg:
             pass
 
     def _img(self, like: Optional[torch.Tensor] = None, coils: bool = False, device=None):
-        shape = (self.B, self.C, self.M, self.N) if coils else (self.B, self.M, self.N)
+        shape = (self.B, self.C) + self.image if coils else (self.B,) + self.image
         dev = device if device is not None else (like.device if like is not None else self.device)
         return torch.empty(shape, dtype=torch.complex64, device=dev,
                            pin_memory=(dev.type == "cpu" and torch.cuda.is_available()))
@@ -163,7 +174,7 @@ class SbPcg:
         return x
 
     def get_k(self) -> torch.Tensor:
-        k = torch.empty((self.B, self.M, self.N), dtype=torch.float64)
+        k = torch.empty((self.B,) + self.image, dtype=torch.float64)
         self._check(_lib.sb_pcg_get_k(self._h, _ptr(k)), "get_k")
         return k
 
@@ -196,9 +207,15 @@ class SbPcg:
         rels = [[rel[j * self.B + b] for b in range(self.B)] for j in range(n_outer)]
         return x, dict(pcg_iters=iters, final_relres=rels, total_ms=log.total_ms)
 
-    def sb_update(self, x, bx, by, bw):
+    def sb_update(self, x, bx, by, bw, bz=None):
+        """One shrink/Bregman step; 3D contexts also take and return b_z (returned last)."""
         bx, by, bw = bx.clone(), by.clone(), bw.clone()
         rhs = torch.empty_like(x)
+        if self.ndim == 3:
+            bz = bz.clone()
+            self._check(_lib.sb_sb_update3(self._h, _ptr(x), _ptr(bx), _ptr(by), _ptr(bz), _ptr(bw),
+                                           _ptr(rhs)), "sb_update3")
+            return bx, by, bw, rhs, bz
         self._check(_lib.sb_sb_update(self._h, _ptr(x), _ptr(bx), _ptr(by), _ptr(bw), _ptr(rhs)),
                     "sb_update")
         return bx, by, bw, rhs

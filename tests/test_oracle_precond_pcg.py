@@ -221,3 +221,30 @@ def test_pcg_scaling_invariance():
     assert out[0].iters == out[1].iters
     np.testing.assert_allclose(out[0].relres, out[1].relres, rtol=1e-9)
     np.testing.assert_allclose(out[1].x * 8.0, out[0].x, rtol=1e-9, atol=1e-12)
+
+
+# ------------------------------------------------------- 3D (BASELINE config 5 geometry)
+@pytest.mark.parametrize("readout_constant", [True, False])
+def test_k_3d_equals_diag_of_dense_K(readout_constant):
+    # k = diag(F_3 A F_3^H) in 3D with complex maps, for a mask constant along d0 (config 5;
+    # then k_c is constant along nu_0 — the plane-marginal form the GPU builds) and for a
+    # generic 3D mask (the oracle's build_k is nd-generic)
+    shape = (4, 4, 6)
+    rng = np.random.default_rng(31)
+    sens = crandn(rng, 2, *shape)
+    if readout_constant:
+        m2 = (rng.random(shape[1:]) < 0.4).astype(np.uint8)
+        m2[0, 0] = 1
+        mask = np.repeat(m2[None], shape[0], axis=0)
+    else:
+        mask = (rng.random(shape) < 0.4).astype(np.uint8)
+        mask[0, 0, 0] = 1
+    mu, lam, gamma = 1.0, 0.05, 0.02
+    A = dense.system_matrix(sens, mask, mu, lam, gamma)
+    F = dense.dft_unitary(shape)
+    K = F @ A @ F.conj().T
+    k = precond.build_k(sens, mask, mu, lam, gamma)
+    np.testing.assert_allclose(k.ravel(), np.diag(K).real, rtol=1e-10, atol=1e-12)
+    if readout_constant:
+        kc = (k - lam * precond.k_d_closed(shape) - gamma) / mu
+        assert np.max(np.abs(kc - kc[:1])) < 1e-12  # constant along nu_0

@@ -23,10 +23,7 @@ ph, sens, mask, noise = bench.make_inputs(a.config, first, per)
 dev = torch.device("cuda", 0)
 ctx = SbPcg(torch.from_numpy(sens).to(torch.complex64).to(dev), torch.from_numpy(mask).to(dev),
             prm.mu, prm.lam, prm.gamma, prm.wavelet_levels)
-yfull = ctx.encode(torch.from_numpy(ph).to(torch.complex64).to(dev), full=True)
-sig = 0.005 * yfull.abs().amax(dim=(1, 2, 3), keepdim=True)
-y = (torch.from_numpy(mask).to(dev).to(torch.complex64).unsqueeze(1) *
-     (yfull + sig * torch.from_numpy(noise).to(torch.complex64).to(dev))).contiguous()
+y = bench.kspace_gpu(ctx, spec, ph, torch.from_numpy(mask).to(dev), noise, dev)
 for i in range(a.warmup + a.steps):
     if i == a.warmup:
         torch.cuda.synchronize()
