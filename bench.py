@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precond", type=int, default=1)
     ap.add_argument("--no-graph", action="store_true")
@@ -72,6 +72,9 @@ def workload(cfg: int, ws: int, rank: int, slices_override: int):
 
 
 def make_inputs(cfg, first, per):
+    if cfg == 5:  # one fully 3D problem (synth.problem3d), complex64 to bound host memory
+        p = synth.problem3d(5, dtype=np.complex64)
+        return p["phantom"][None], p["sens"][None], p["mask"][None], p["noise"][None]
     if cfg == 4:  # readout planes of one 3D volume, shared 2D mask (synth.problem_c4)
         p = synth.problem_c4(range(first, first + per))
         return p["phantom"], p["sens"], p["mask"], p["noise"]
@@ -157,10 +160,24 @@ def run_reference(args):
         if rank != 0:
             dist.barrier()
             return
-    from oracle import sb
     spec, per, first = workload(args.config, 1, 0, args.slices)
-    p, y = oracle_problem(args.config, first)
     prm = spec.params
+    if args.config == 5:
+        cb = cpu_baseline_3d(args.config, args.precond)
+        value = cb["value"]
+        line = {
+            "impl": "reference", "metric": METRIC, "value": value, "unit": "PCG iters/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded phantom/coils/mask)",
+            "config": {"workload": spec.name, "sample": cb["sample"]},
+            "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": "PCG iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line))
+        return
+    from oracle import sb
+    p, y = oracle_problem(args.config, first)
 
     def sample():
         t = time.perf_counter()
@@ -206,9 +223,42 @@ def oracle_problem(cfg, s):
     return p, problems.make_kspace(p["phantom"], p["sens"], p["mask"], p["noise"])
 
 
+def cpu_baseline_3d(cfg, precond):
+    """Config 5: one oracle PCG iteration at 192^3 x 32 coils is ~7 min of single-thread numpy
+    (64 own-FFT 3D transforms), so the bounded sample times ONE coil's data-term pair
+    E_c^H E_c p plus the regulariser, and one M^{-1} application, and extrapolates
+    t_iter = C * t_coil + t_rest (labelled as such)."""
+    from oracle import ops, precond as opre
+    p = synth.problem3d(cfg, dtype=np.complex64)
+    spec = synth.CONFIGS[cfg]
+    prm = spec.params
+    s0 = p["sens"][:1].astype(np.complex128)
+    x = p["phantom"].astype(np.complex128)
+    t = time.perf_counter()
+    ops.data_normal(x, s0, p["mask"])
+    t_coil = time.perf_counter() - t
+    t = time.perf_counter()
+    ops.tv_normal(x)
+    t_reg = time.perf_counter() - t
+    t_pre = 0.0
+    if precond:
+        kd = opre.k_d_closed(spec.shape)
+        k = prm.mu * 0.5 + prm.lam * kd + prm.gamma  # stand-in diagonal: M^{-1} cost only
+        t = time.perf_counter()
+        opre.apply_Minv(x, k)
+        t_pre = time.perf_counter() - t
+    t_iter = spec.coils * t_coil + t_reg + t_pre
+    return {"value": 1.0 / t_iter, "unit": "PCG iters/s", "cores": 1, "kind": "oracle",
+            "sample": f"extrapolated: 1 coil data-term pair ({t_coil:.1f} s) x {spec.coils} coils + "
+                      f"regulariser ({t_reg:.1f} s) + one M^-1 ({t_pre:.1f} s) = {t_iter:.0f} s per PCG "
+                      f"iteration at 192^3, numpy fp64 single thread (own FFT)"}
+
+
 def cpu_baseline_sample(cfg, precond):
     """Oracle PCG iterations/s on a bounded sample: the first 2 SB outer iterations of slice 0
     (about 10-30 s of single-threaded numpy work at config 2)."""
+    if cfg == 5:
+        return cpu_baseline_3d(cfg, precond)
     from oracle import sb
     spec = synth.CONFIGS[cfg]
     p, y = oracle_problem(cfg, 0)
@@ -235,7 +285,7 @@ def kspace_gpu(ctx, spec, phantom, mask_d, noise, dev):
         sigma = 0.005 * yfull.abs().amax()
         mask_c = mask_d.to(torch.complex64)[None, None]
     else:
-        sigma = 0.005 * yfull.abs().amax(dim=(1, 2, 3), keepdim=True)
+        sigma = 0.005 * yfull.abs().flatten(1).amax(dim=1).view((-1,) + (1,) * (yfull.dim() - 1))
         mask_c = mask_d.to(torch.complex64).unsqueeze(1)
     yfull.add_(sigma * torch.from_numpy(noise).to(torch.complex64).to(dev))
     yfull.mul_(mask_c)
@@ -262,7 +312,7 @@ def run_ours(args):
     mask_d = torch.from_numpy(mask).to(dev)
     ctx = SbPcg(sens_d, mask_d, prm.mu, prm.lam, prm.gamma, prm.wavelet_levels)
     y_d = kspace_gpu(ctx, spec, phantom, mask_d, noise, dev)
-    out = torch.empty((per, spec.shape[0], spec.shape[1]), dtype=torch.complex64, device=dev)
+    out = torch.empty((per,) + tuple(spec.shape), dtype=torch.complex64, device=dev)
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
     use_graph = not args.no_graph
 
@@ -374,6 +424,10 @@ def run_ours(args):
         cpu = cpu_baseline_sample(args.config, args.precond)
 
     if rank == 0:
+        mask_desc = {"lines": "VD lines R=%d, %d-line centre" % (spec.accel, spec.center),
+                     "random2d": "shared 2D VD random R=%d, %dx%d centre" % (spec.accel, spec.center, spec.center),
+                     "pe2d": "2D VD phase-encode R=%d, %dx%d centre, readout fully sampled"
+                             % (spec.accel, spec.center, spec.center)}[spec.mask_kind]
         line = {
             "metric": METRIC, "value": value, "unit": "PCG iters/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -381,8 +435,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "c64 (fp32 complex; Lambda built in f64)",
             "data": "synthetic (seeded phantoms, coil maps, masks; k-space by sb_encode)",
             "config": {"workload": spec.name, "problems_per_gpu": per, "shape": list(spec.shape),
-                       "coils": spec.coils, "mask": ("VD lines R=%d, %d-line centre" % (spec.accel, spec.center)) if spec.mask_kind == "lines"
-                       else ("shared 2D VD random R=%d, %dx%d centre" % (spec.accel, spec.center, spec.center)),
+                       "coils": spec.coils, "mask": mask_desc,
                        "mu": prm.mu, "lambda": prm.lam, "gamma": prm.gamma, "n_outer": prm.n_outer,
                        "pcg_eps": prm.eps, "pcg_max_iters": prm.max_iters,
                        "precond": "circulant" if args.precond else "none",
@@ -391,7 +444,8 @@ def run_ours(args):
                        "loop": "CUDA graph, conditional while node" if use_graph else "eager"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "k1_matvec (fused coil FFT matvec)",
+                         "kernel": ("k1_matvec (fused coil FFT matvec, line-mask 1D FFTs)" if spec.mask_kind == "lines"
+                                    else "kp_plane (cluster plane matvec: per-coil 2D FFT via DSMEM)"),
                          "kernel_avg_us": k_avg_s * 1e6, "kernel_launches_timed": k_n,
                          "alg_bytes_per_launch": k_bytes},
             "cpu_baseline": cpu,

@@ -8,9 +8,8 @@
 //
 // Separable (line) masks (r depends on the d0 row only): with F = F_0 (x) F_1
 // the data term is exactly  F_0^H R_0 F_0 (x) I  per coil, so each coil needs one length-M
-// FFT pair down every column, scaled by r/M.
-// Generic masks: passes A/B (k_passes.cu) leave r . F(s_c p) transformed along d1 back to
-// the (k0, n1) domain in tmpc, and this kernel only does the column IFFT.
+// FFT pair down every column, scaled by r/M.  Other
+// masks take the plane-cluster kernel K1P (k_plane.cu).
 //
 // Per coil: the s_c tile (M x W complex64) arrives by 3D TMA into a 2-stage ring (mbarrier
 // complete_tx); the column FFT is register resident (four-step, fft_core.cuh); the coil
@@ -26,7 +25,7 @@ namespace cg = cooperative_groups;
 
 namespace sbk {
 
-template <int M, int W, int MODE, bool SEP>
+template <int M, int W, int MODE>
 __global__ void __launch_bounds__(Split<M>::N2* W)
     k1_matvec(const __grid_constant__ CUtensorMap tmap, const K1Args a) {
   constexpr int N1 = Split<M>::N1, N2 = Split<M>::N2;
@@ -66,7 +65,7 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
   }
   for (int i = tid; i < M; i += NT) {
     tw[i] = a.tw[i];
-    if constexpr (SEP) rm[i] = a.rmask[(size_t)b * a.rmask_bstride + i];
+    rm[i] = a.rmask[(size_t)b * a.rmask_bstride + i];
   }
   __syncthreads();
   if (tid == 0) {
@@ -181,35 +180,22 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
       const int row = natidx<M>(j, n1);
       s[n1] = sc[row * W + l];
     }
-    if constexpr (SEP) {
 #pragma unroll
-      for (int n1 = 0; n1 < N1; ++n1) {
-        const int row = natidx<M>(j, n1);
-        v[n1] = cmul(s[n1], pt[row * PW + l + 1]);
-      }
-      fft_fwd<M, Lay>(v, xch, tw, j, l);
-      // every thread has read ring[stage] before the barrier inside fft_fwd
-      if (tid == 0 && ci + 2 < ncoil) {
-        const int c = g + (ci + 2) * G;
-        mbar_expect_tx(&bar[stage], TILE * 8);
-        tma_load_3d(ring + stage * TILE, &tmap, 2 * col0, 0, b * a.C + c, &bar[stage]);
-      }
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const int row = natidx<M>(j, n1);
+      v[n1] = cmul(s[n1], pt[row * PW + l + 1]);
+    }
+    fft_fwd<M, Lay>(v, xch, tw, j, l);
+    // every thread has read ring[stage] before the barrier inside fft_fwd
+    if (tid == 0 && ci + 2 < ncoil) {
+      const int c = g + (ci + 2) * G;
+      mbar_expect_tx(&bar[stage], TILE * 8);
+      tma_load_3d(ring + stage * TILE, &tmap, 2 * col0, 0, b * a.C + c, &bar[stage]);
+    }
 #pragma unroll
-      for (int q = 0; q < N1; ++q) {
-        const float r = rm[specidx<M>(j, q)];
-        v[q] = make_float2(v[q].x * r, v[q].y * r);
-      }
-    } else {
-      const int c = g + ci * G;
-      const float2* tc = a.tmpc + ((size_t)b * a.C + c) * img;
-#pragma unroll
-      for (int q = 0; q < N1; ++q) v[q] = tc[(size_t)specidx<M>(j, q) * N + col0 + l];
-      __syncthreads();  // all threads read ring[stage]
-      if (tid == 0 && ci + 2 < ncoil) {
-        const int c2 = g + (ci + 2) * G;
-        mbar_expect_tx(&bar[stage], TILE * 8);
-        tma_load_3d(ring + stage * TILE, &tmap, 2 * col0, 0, b * a.C + c2, &bar[stage]);
-      }
+    for (int q = 0; q < N1; ++q) {
+      const float r = rm[specidx<M>(j, q)];
+      v[q] = make_float2(v[q].x * r, v[q].y * r);
     }
     fft_inv<M, Lay>(v, xch, tw, j, l);
 #pragma unroll
@@ -218,7 +204,6 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
       acc[n1].x += t.x;
       acc[n1].y += t.y;
     }
-    if constexpr (!SEP) __syncthreads();  // xch reuse between consecutive inverses
   }
 
   // ---- coil-group reduction (DSMEM) + epilogue
@@ -324,9 +309,9 @@ constexpr size_t k1_smem() {
          (M + (M & 1)) * sizeof(float) + 2 * sizeof(uint64_t);
 }
 
-template <int M, int W, int MODE, bool SEP>
+template <int M, int W, int MODE>
 static cudaError_t launch_k1_t(const K1Args& a, const CUtensorMap* tmap, int G, cudaStream_t st) {
-  auto kern = k1_matvec<M, W, MODE, SEP>;
+  auto kern = k1_matvec<M, W, MODE>;
   constexpr size_t smem = k1_smem<M, W>();
   static bool attr_done = false;  // per instantiation
   if (!attr_done) {
@@ -338,29 +323,20 @@ static cudaError_t launch_k1_t(const K1Args& a, const CUtensorMap* tmap, int G, 
 }
 
 template <int M, int W>
-static cudaError_t launch_k1_mw(int mode, bool sep, const K1Args& a, const CUtensorMap* tmap, int G,
-                                cudaStream_t st) {
-  if (sep) {
-    switch (mode) {
-      case K1_APPLY: return launch_k1_t<M, W, K1_APPLY, true>(a, tmap, G, st);
-      case K1_PCG: return launch_k1_t<M, W, K1_PCG, true>(a, tmap, G, st);
-      default: return launch_k1_t<M, W, K1_RESID, true>(a, tmap, G, st);
-    }
-  } else {
-    switch (mode) {
-      case K1_APPLY: return launch_k1_t<M, W, K1_APPLY, false>(a, tmap, G, st);
-      case K1_PCG: return launch_k1_t<M, W, K1_PCG, false>(a, tmap, G, st);
-      default: return launch_k1_t<M, W, K1_RESID, false>(a, tmap, G, st);
-    }
+static cudaError_t launch_k1_mw(int mode, const K1Args& a, const CUtensorMap* tmap, int G, cudaStream_t st) {
+  switch (mode) {
+    case K1_APPLY: return launch_k1_t<M, W, K1_APPLY>(a, tmap, G, st);
+    case K1_PCG: return launch_k1_t<M, W, K1_PCG>(a, tmap, G, st);
+    default: return launch_k1_t<M, W, K1_RESID>(a, tmap, G, st);
   }
 }
 
 template <int M>
-static cudaError_t launch_k1_m(int mode, bool sep, const K1Args& a, const CUtensorMap* tmap, int W, int G,
+static cudaError_t launch_k1_m(int mode, const K1Args& a, const CUtensorMap* tmap, int W, int G,
                                cudaStream_t st) {
   switch (W) {
-    case 4: return launch_k1_mw<M, 4>(mode, sep, a, tmap, G, st);
-    case 8: return launch_k1_mw<M, 8>(mode, sep, a, tmap, G, st);
+    case 4: return launch_k1_mw<M, 4>(mode, a, tmap, G, st);
+    case 8: return launch_k1_mw<M, 8>(mode, a, tmap, G, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -372,16 +348,16 @@ bool k1_supported(int M, int N) {
 
 int k1_default_W(int M, int N) { return (N % 8 == 0) ? 8 : 4; }
 
-cudaError_t launch_k1(int mode, bool separable, const K1Args& a, const CUtensorMap* tmap, int W, int G,
+cudaError_t launch_k1(int mode, const K1Args& a, const CUtensorMap* tmap, int W, int G,
                       cudaStream_t st) {
   if (a.M % G != 0 || a.N % W != 0 || G > 8) return cudaErrorInvalidValue;
   switch (a.M) {
-    case 8: return launch_k1_m<8>(mode, separable, a, tmap, W, G, st);
-    case 16: return launch_k1_m<16>(mode, separable, a, tmap, W, G, st);
-    case 32: return launch_k1_m<32>(mode, separable, a, tmap, W, G, st);
-    case 64: return launch_k1_m<64>(mode, separable, a, tmap, W, G, st);
-    case 128: return launch_k1_m<128>(mode, separable, a, tmap, W, G, st);
-    case 256: return launch_k1_m<256>(mode, separable, a, tmap, W, G, st);
+    case 8: return launch_k1_m<8>(mode, a, tmap, W, G, st);
+    case 16: return launch_k1_m<16>(mode, a, tmap, W, G, st);
+    case 32: return launch_k1_m<32>(mode, a, tmap, W, G, st);
+    case 64: return launch_k1_m<64>(mode, a, tmap, W, G, st);
+    case 128: return launch_k1_m<128>(mode, a, tmap, W, G, st);
+    case 256: return launch_k1_m<256>(mode, a, tmap, W, G, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -4,7 +4,7 @@
 //     IFFT), K2c (column IFFT, fused <r, z>) — Lambda^{-1} = 1/(N k) folds the 1/N;
 //   * the encoding operator E_c = R F S_c and its adjoint (Alg. 1 step 4);
 //   * SB init: u_1 = sum_c S_c^H F^H y_c and x^[1] = RSS (reading A12);
-//   * generic (non-separable mask) matvec passes A and B;
+//   * plain column FFTs/IFFTs of coil stacks (the d0 transform of 3D E and E^H);
 //   * the no-preconditioner step and the PCG exit fixup.
 // Column passes: one CTA = W columns x all M rows of one image, threads (j, col) with col
 // fastest (coalesced rows of W*8 bytes).  Row passes: one CTA = LINES rows, threads
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(ColCfg<M, W_>::NT) k_col(const PassArgs a) {
 
   // image / problem index
   int b, c = 0;
-  if constexpr (KIND == P_ENC_COL || KIND == P_GEN_A_COL || KIND == P_COL_FWD || KIND == P_COL_INV) {
+  if constexpr (KIND == P_ENC_COL || KIND == P_COL_FWD || KIND == P_COL_INV) {
     b = blockIdx.y / a.C;
     c = blockIdx.y % a.C;
   } else {
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(ColCfg<M, W_>::NT) k_col(const PassArgs a) {
   pdl_trigger();
   pdl_wait();
 
-  if constexpr (KIND == P_PRE_A_FWD_COL || KIND == P_PRE_C_INV_COL || KIND == P_GEN_A_COL) {
+  if constexpr (KIND == P_PRE_A_FWD_COL || KIND == P_PRE_C_INV_COL) {
     if (!slice_active(a, b)) {
       if constexpr (KIND == P_PRE_C_INV_COL) {
         if (a.L.scal != nullptr && a.mode >= 0 && blockIdx.x == 0 && tid == 0) slice_arrive(a.L);
@@ -142,37 +142,12 @@ __global__ void __launch_bounds__(ColCfg<M, W_>::NT) k_col(const PassArgs a) {
         }
       }
     }
-  } else if constexpr (KIND == P_ENC_COL || KIND == P_GEN_A_COL) {
+  } else if constexpr (KIND == P_ENC_COL) {
     const float2* sc = a.sens + ((size_t)b * a.C + c) * img;
-    const float2* pin = a.a0;
-    double beta = 0.0;
-    bool first = true;
-    int pidx = 0;
-    if constexpr (KIND == P_GEN_A_COL) {
-      if (a.mode == 1) {
-        const Scal& s = a.L.scal[b];
-        const int k = s.iter + 1;
-        first = (k == 1);
-        pidx = k & 1;
-        beta = s.beta;
-      }
-    }
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) {
       const size_t gi = boff + (size_t)natidx<M>(j, n1) * N + col;
-      float2 p;
-      if (KIND == P_GEN_A_COL && a.mode == 1) {
-        const float2 zz = a.z[gi];
-        if (first) {
-          p = zz;
-        } else {
-          const float2 po = (pidx ? a.pbuf0 : a.pbuf1)[gi];
-          p = make_float2(zz.x + (float)beta * po.x, zz.y + (float)beta * po.y);
-        }
-      } else {
-        p = pin[gi];
-      }
-      v[n1] = cmul(sc[gi - boff], p);
+      v[n1] = cmul(sc[gi - boff], a.a0[gi]);
     }
     fft_fwd<M, typename C::Lay>(v, xch, tw, j, l);
     float2* t = a.tmp + ((size_t)b * a.C + c) * img;
@@ -254,9 +229,6 @@ __global__ void __launch_bounds__(RowCfg<N, LINES_>::NT) k_row(const PassArgs a)
   } else {
     b = blockIdx.y / a.C;
     c = blockIdx.y % a.C;
-    if constexpr (KIND == P_GEN_B_ROW) {
-      if (a.mode == 1 && !slice_active(a, b)) return;
-    }
   }
   __syncthreads();
   const bool in_range = row < M;
@@ -275,22 +247,6 @@ __global__ void __launch_bounds__(RowCfg<N, LINES_>::NT) k_row(const PassArgs a)
     fft_fwd<N, typename R::Lay>(v, xch, tw, j, line);
 #pragma unroll
     for (int s = 0; s < N1; ++s) v[s] = make_float2(v[s].x * lv[s], v[s].y * lv[s]);
-    fft_inv<N, typename R::Lay>(v, xch, tw, j, line);
-    if (in_range) {
-#pragma unroll
-      for (int n1 = 0; n1 < N1; ++n1) t[natidx<N>(j, n1)] = v[n1];
-    }
-  } else if constexpr (KIND == P_GEN_B_ROW) {
-    float2* t = a.tmp + ((size_t)b * a.C + c) * img + (size_t)rr * N;
-    const uint8_t* mk = a.mask + (size_t)b * a.mask_bstride + (size_t)rr * N;
-#pragma unroll
-    for (int n1 = 0; n1 < N1; ++n1) v[n1] = t[natidx<N>(j, n1)];
-    fft_fwd<N, typename R::Lay>(v, xch, tw, j, line);
-#pragma unroll
-    for (int s = 0; s < N1; ++s) {
-      const float f = mk[specidx<N>(j, s)] ? a.scale : 0.f;
-      v[s] = make_float2(v[s].x * f, v[s].y * f);
-    }
     fft_inv<N, typename R::Lay>(v, xch, tw, j, line);
     if (in_range) {
 #pragma unroll
@@ -447,7 +403,7 @@ constexpr int kFill = 2 * 148;
 
 template <int M, int KIND>
 static cudaError_t launch_col_t(const PassArgs& a, cudaStream_t st) {
-  const int nimg = (KIND == P_ENC_COL || KIND == P_GEN_A_COL || KIND == P_COL_FWD || KIND == P_COL_INV) ? a.B * a.C : a.B;
+  const int nimg = (KIND == P_ENC_COL || KIND == P_COL_FWD || KIND == P_COL_INV) ? a.B * a.C : a.B;
   constexpr int WS = (32 / Split<M>::N2) > 2 ? 32 / Split<M>::N2 : 2;  // >= one warp per CTA
   if (WS < 8 && (a.N / 8) * nimg < kFill) {
     return launch_ex(k_col<M, (WS < 8 ? WS : 8), KIND>, dim3(a.N / WS, nimg), dim3(ColCfg<M, (WS < 8 ? WS : 8)>::NT),
@@ -509,8 +465,6 @@ cudaError_t launch_pass(int kind, const PassArgs& a, cudaStream_t st) {
     case P_ENC_ROW: return row_dispatch<P_ENC_ROW>(a, st);
     case P_ADJ_ROW: return row_dispatch<P_ADJ_ROW>(a, st);
     case P_ADJ_COL: return col_dispatch<P_ADJ_COL>(a, st);
-    case P_GEN_A_COL: return col_dispatch<P_GEN_A_COL>(a, st);
-    case P_GEN_B_ROW: return row_dispatch<P_GEN_B_ROW>(a, st);
     case P_COL_FWD: return col_dispatch<P_COL_FWD>(a, st);
     case P_COL_INV: return col_dispatch<P_COL_INV>(a, st);
     case P_NOPRE: {

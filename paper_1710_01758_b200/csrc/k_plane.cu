@@ -112,6 +112,11 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T) kp_plane(const KPArgs 
     alpha_prev = s.alpha;
   } else if constexpr (MODE == KP_PRECOND) {
     if (a.L.scal != nullptr && __ldcg(&a.L.scal[b].active) == 0) return;
+  } else if constexpr (MODE == KP_PRE2D) {
+    if (a.L.scal != nullptr && a.pmode >= 0 && __ldcg(&a.L.scal[b].active) == 0) {
+      if (g == 0 && tid == 0) slice_arrive(a.L);  // uniform over the cluster
+      return;
+    }
   }
   if (MATVEC && g == 0 && xpl == 0 && tid == 0 && a.L.cnt != nullptr) atomicAdd(&a.L.cnt->k1_problems, 1ull);
   __syncthreads();
@@ -171,7 +176,29 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T) kp_plane(const KPArgs 
     acc[i] = make_float2(0.f, 0.f);
     rss[i] = 0.f;
   }
-  const int ncoil = (MODE == KP_PRECOND) ? 1 : a.C;
+  const int ncoil = (MODE == KP_PRECOND || MODE == KP_PRE2D) ? 1 : a.C;
+  // PRE2D: r_k = r_{k-1} - alpha_k q_k, kept in registers for <r, z>
+  float2 rk[MODE == KP_PRE2D ? N1 : 1];
+  double drr = 0.0, drz = 0.0;
+  if constexpr (MODE == KP_PRE2D) {
+    const double alpha = (a.pmode == 1) ? a.L.scal[b].alpha : 0.0;
+    float2 qq[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const size_t gi = gidx(r, N2 * n1 + j);
+      rk[n1] = a.vin[gi];
+      qq[n1] = (a.pmode == 1) ? a.qv[gi] : make_float2(0.f, 0.f);
+    }
+    if (a.pmode == 1) {
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) {
+        rk[n1].x -= (float)alpha * qq[n1].x;
+        rk[n1].y -= (float)alpha * qq[n1].y;
+        a.rout[gidx(r, N2 * n1 + j)] = rk[n1];
+        drr += (double)rk[n1].x * rk[n1].x + (double)rk[n1].y * rk[n1].y;
+      }
+    }
+  }
   const uint8_t* mk = a.mask + (size_t)b * a.mask_bstride;
   float2 colv[NYL];
 
@@ -185,6 +212,8 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T) kp_plane(const KPArgs 
         const int z = N2 * n1 + j;
         if constexpr (MODE == KP_PRECOND) {
           v[n1] = a.tmp[gidx(r, z)];
+        } else if constexpr (MODE == KP_PRE2D) {
+          v[n1] = rk[n1];
         } else {
           s[n1] = a.sens[soff + (size_t)(G * r + g) * NZ + z];
           v[n1] = cmul(s[n1], pt[r * NZ + z]);
@@ -234,7 +263,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T) kp_plane(const KPArgs 
           for (int ka = 0; ka < G; ++ka) {
             const int ky = kb + NYL * ka;
             float f;
-            if constexpr (MODE == KP_PRECOND) {
+            if constexpr (MODE == KP_PRECOND || MODE == KP_PRE2D) {
               f = a.lam_inv[boff + (size_t)xpl * PN + (size_t)ky * NZ + kz];
             } else if constexpr (MODE == KP_ENCODE) {
               f = (a.full || mk[ky * NZ + kz]) ? a.scale : 0.f;
@@ -280,6 +309,12 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T) kp_plane(const KPArgs 
     if constexpr (MODE == KP_PRECOND) {
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) a.tmp[gidx(r, N2 * n1 + j)] = v[n1];
+    } else if constexpr (MODE == KP_PRE2D) {
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) {
+        a.zout[gidx(r, N2 * n1 + j)] = v[n1];
+        drz += (double)rk[n1].x * v[n1].x + (double)rk[n1].y * v[n1].y;
+      }
     } else if constexpr (MODE == KP_ADJOINT) {
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) {
@@ -307,6 +342,28 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T) kp_plane(const KPArgs 
       a.out[gi] = acc[n1];
       if (a.out2 != nullptr) a.out2[gi] = make_float2(sqrtf(rss[n1]), 0.f);
     }
+  }
+  if constexpr (MODE == KP_PRE2D) {
+    if (a.L.scal == nullptr || a.pmode < 0) return;
+    const double s0 = block_sum(drz, red);
+    const double s1 = block_sum(drr, red);
+    const bool last = publish_and_check_last(s0, s1, a.P, b, xpl * G + g, planes * G, &lastflag);
+    if (!last) return;
+    if (tid < 32 || T < 32) {
+      const double trz = warp_sum_partials(a.P.p0 + (size_t)b * a.P.cap, planes * G);
+      const double trr = warp_sum_partials(a.P.p1 + (size_t)b * a.P.cap, planes * G);
+      if (tid == 0) {
+        if (a.pmode == 1) {
+          fin_rr(a.L, b, trr);                                   // ||r_k||/||b|| stop test
+          if (a.L.scal[b].active) fin_rho(a.L, b, trz, false);  // rho', beta, max-iter stop
+        } else {
+          fin_rho(a.L, b, trz, true);                            // rho_0
+        }
+        a.P.cnt[b] = 0;
+        slice_arrive(a.L);
+      }
+    }
+    return;
   }
   if constexpr (!MATVEC) return;
 
@@ -437,6 +494,7 @@ template <int NY, int NZ>
 static cudaError_t kp_matvec_modes(int mode, const KPArgs& a, cudaStream_t st) {
   constexpr int G = PlaneG<NY>::value;
   switch (mode) {
+    case KP_PRE2D: return kp_launch<NY, NZ, G, KP_PRE2D>(a, st);
     case KP_APPLY: return kp_launch<NY, NZ, G, KP_APPLY>(a, st);
     case KP_PCG: return kp_launch<NY, NZ, G, KP_PCG>(a, st);
     case KP_RESID: return kp_launch<NY, NZ, G, KP_RESID>(a, st);
@@ -463,9 +521,11 @@ static cudaError_t kp_all_modes(int mode, const KPArgs& a, cudaStream_t st) {
 #else
 // 2D problems with a non-separable mask (matvec modes; encode/adjoint/preconditioner use the
 // column/row passes of k_passes.cu)
-#define SBK_PLANE_SIZES(X) \
-  X(8, 8) X(16, 16) X(16, 32) X(32, 16) X(32, 32) X(64, 64) X(64, 128) X(128, 64) X(128, 128) \
-  X(128, 256) X(256, 128) X(256, 256)
+#define SBK_PLANE_SIZES(X)                                                                       \
+  X(8, 8) X(8, 16) X(8, 32) X(8, 64) X(16, 8) X(16, 16) X(16, 32) X(16, 64) X(16, 128) X(16, 256)   \
+  X(32, 8) X(32, 16) X(32, 32) X(32, 64) X(32, 128) X(32, 256) X(64, 8) X(64, 16) X(64, 32)         \
+  X(64, 64) X(64, 128) X(64, 256) X(128, 8) X(128, 16) X(128, 32) X(128, 64) X(128, 128)             \
+  X(128, 256) X(256, 8) X(256, 16) X(256, 32) X(256, 64) X(256, 128) X(256, 256)
 #define SBK_PLANE_FN kp_matvec_modes
 #define SBK_PLANE_ENTRY launch_kp2
 #define SBK_PLANE_SUPP kp2_supported

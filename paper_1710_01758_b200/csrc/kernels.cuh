@@ -11,9 +11,8 @@ enum K1Mode { K1_APPLY = 0, K1_PCG = 1, K1_RESID = 2 };
 struct K1Args {
   int B, C, M, N;
   float mu, lam, gam;
-  const float* rmask;      // [B or 1][M] = r/M (separable) ; or null (generic)
+  const float* rmask;      // [B or 1][M] = r/M (line masks)
   int rmask_bstride;       // M or 0
-  const float2* tmpc;      // generic path: [B][C][M][N] spectra after pass B (layout: row = k0)
   // APPLY: vin -> out = A vin.   RESID: vin = x, out = r.   PCG: out = q.
   const float2* vin;
   float2* out;
@@ -120,7 +119,8 @@ struct SbArgs {
 };
 
 // Plane kernels (k_plane*.cu): one G-CTA cluster per NY x NZ plane, DSMEM-exchanged 2D FFT.
-enum KPMode { KP_APPLY = 0, KP_PCG = 1, KP_RESID = 2, KP_PRECOND = 3, KP_ENCODE = 4, KP_ADJOINT = 5 };
+enum KPMode { KP_APPLY = 0, KP_PCG = 1, KP_RESID = 2, KP_PRECOND = 3, KP_ENCODE = 4, KP_ADJOINT = 5,
+              KP_PRE2D = 6 };
 struct KPArgs {
   int B, C, planes, NY, NZ;  // image = planes x NY x NZ per problem (2D: planes = 1)
   int d3;                    // 1: 3D problem (7-point Laplacian across planes)
@@ -151,6 +151,11 @@ struct KPArgs {
   int update_u;
   float eps;
   int maxit;
+  // PRE2D (fused 2D preconditioner): r -= alpha q ; z = F^H Lambda^{-1} F r ; ||r||^2, <r, z>
+  const float2* qv;
+  float2* rout;
+  float2* zout;
+  int pmode;                 // -1 standalone apply, 0 PCG init, 1 PCG iteration
   Loop L;
   Partials P;
 };
@@ -188,7 +193,7 @@ inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size
 }
 
 // launchers (return cudaError_t of the launch)
-cudaError_t launch_k1(int mode, bool separable, const K1Args& a, const CUtensorMap* tmap, int W, int G,
+cudaError_t launch_k1(int mode, const K1Args& a, const CUtensorMap* tmap, int W, int G,
                       cudaStream_t st);
 bool k1_supported(int M, int N);
 int k1_default_W(int M, int N);
@@ -201,8 +206,7 @@ enum PassKind {
   P_ENC_ROW = 4,         // encode: row FFT fwd, x mask / sqrt(N) -> y
   P_ADJ_ROW = 5,         // adjoint/init: y masked, row IFFT -> tmp[b][c]
   P_ADJ_COL = 6,         // adjoint/init: col IFFT, sum_c conj(s_c) . / sqrt(N) (+ RSS)
-  P_GEN_A_COL = 7,       // generic matvec: (p-update) ; t_c = s_c p ; col FFT fwd -> tmp[b][c]
-  P_GEN_B_ROW = 8,       // generic matvec: row FFT, x mask/N, row IFFT
+  // 7, 8: retired (non-separable masks use the plane kernel K1P)
   P_NOPRE = 9,           // no preconditioner: r -= alpha q ; z = r ; partials
   P_FIXUP = 10,          // x += alpha p (pending) / x = 0
   P_COL_FWD = 11,        // o0[b][c] = colFFT(a0[b][c]) * scale   (3D: the d0 transform of E)

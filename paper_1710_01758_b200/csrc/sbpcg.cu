@@ -49,6 +49,7 @@ struct sb_ctx {
   // M = D0 (the readout, column-pass length) and N = D1*D2 (column-pass columns)
   int ndim = 2, D0 = 0, D1 = 0, D2 = 1;
   bool plane = false;           // K1P plane kernels (2D non-separable masks, or 3D)
+  bool pre2d = false;           // 2D preconditioner as one K1P cluster kernel (KP_PRE2D)
   uint8_t* pmask = nullptr;     // 3D: the plane mask [Bm][D1*D2] (mask constant along d0)
   float2 *tw_y = nullptr, *tw_z = nullptr;  // plane twiddles (3D: D1, D2)
   double2 *twd_y = nullptr, *twd_z = nullptr;
@@ -188,7 +189,6 @@ static K1Args base_k1(sb_ctx* c) {
   a.gam = c->gam;
   a.rmask = c->rowmask;
   a.rmask_bstride = c->mask_shared ? 0 : c->M;
-  a.tmpc = c->tmpc;
   a.P = c->P;
   a.tw = c->tw_m;
   return a;
@@ -262,7 +262,7 @@ static sb_status run_k1(sb_ctx* c, int mode, const K1Args& a, cudaStream_t st) {
     e0 = (int)c->evnext;
     CK(cudaEventRecord(ev_get(c), st));
   }
-  CK(launch_k1(mode, c->separable, a, &c->tmap, c->W, c->G, st));
+  CK(launch_k1(mode, a, &c->tmap, c->W, c->G, st));
   if (c->timing) {
     int e1 = (int)c->evnext;
     CK(cudaEventRecord(ev_get(c), st));
@@ -317,16 +317,6 @@ static sb_status seq_apply(sb_ctx* c, const float2* v, float2* out, cudaStream_t
     k.out = out;
     return run_kp(c, KP_APPLY, k, st);
   }
-  if (!c->separable) {
-    PassArgs pa = base_pass(c);
-    pa.a0 = v;
-    pa.tmp = c->tmpc;
-    pa.mode = 0;
-    pa.scale = 1.0f / (float)c->img;
-    sb_status s;
-    if ((s = run_pass(c, P_GEN_A_COL, pa, st))) return s;
-    if ((s = run_pass(c, P_GEN_B_ROW, pa, st))) return s;
-  }
   K1Args a = base_k1(c);
   a.vin = v;
   a.out = out;
@@ -350,16 +340,6 @@ static sb_status seq_resid(sb_ctx* c, Loop L, const float2* bgiven, bool recon, 
     k.maxit = maxit;
     k.L = L;
     return run_kp(c, KP_RESID, k, st);
-  }
-  if (!c->separable) {
-    PassArgs pa = base_pass(c);
-    pa.a0 = c->x;
-    pa.tmp = c->tmpc;
-    pa.mode = 0;
-    pa.scale = 1.0f / (float)c->img;
-    sb_status s;
-    if ((s = run_pass(c, P_GEN_A_COL, pa, st))) return s;
-    if ((s = run_pass(c, P_GEN_B_ROW, pa, st))) return s;
   }
   K1Args a = base_k1(c);
   a.vin = c->x;
@@ -391,6 +371,16 @@ static sb_status seq_precond(sb_ctx* c, Loop L, int precond, int mode, const flo
     pa.o1 = c->z;
     return run_pass(c, P_NOPRE, pa, st);
   }
+  if (c->pre2d) {  // one cluster kernel: r -= alpha q, ||r||^2, z = F^H Lambda^{-1} F r, <r, z>
+    KPArgs k = base_kp(c);
+    k.vin = rin;
+    k.qv = c->q;
+    k.rout = c->r;
+    k.zout = zout;
+    k.pmode = mode;
+    k.L = L;
+    return run_kp(c, KP_PRE2D, k, st);
+  }
   pa.a0 = rin;
   pa.a1 = c->q;
   pa.o0 = c->r;
@@ -420,15 +410,6 @@ static sb_status seq_body(sb_ctx* c, Loop L, int precond, cudaStream_t st, int* 
     if ((s = seq_precond(c, L, precond, 1, c->r, c->z, st))) return s;
     if (nk) *nk = (int)c->launches - n0;
     return SB_OK;
-  }
-  if (!c->separable) {
-    PassArgs pa = base_pass(c);
-    pa.L = L;
-    pa.mode = 1;
-    pa.tmp = c->tmpc;
-    pa.scale = 1.0f / (float)c->img;
-    if ((s = run_pass(c, P_GEN_A_COL, pa, st))) return s;
-    if ((s = run_pass(c, P_GEN_B_ROW, pa, st))) return s;
   }
   K1Args a = base_k1(c);
   a.z = c->z;
@@ -951,7 +932,13 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
         rm[(size_t)b * M + i] = row[0] ? 1.0f / (float)M : 0.f;
       }
     c->separable = sep;
-    c->plane = !sep && kp2_supported((int)M, (int)N);
+    c->plane = !sep;
+    if (!sep && !kp2_supported((int)M, (int)N)) {  // non-separable masks need the plane kernel
+      c->err = "non-separable 2D mask: plane size not instantiated in k_plane.cu";
+      sb_pcg_destroy(c);
+      return SB_E_UNSUPPORTED_SIZE;
+    }
+    c->pre2d = kp2_supported((int)M, (int)N) && env_flag("SBPCG_PRE2D", true);
     if (sep && cudaMemcpy(c->rowmask, rm.data(), rm.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(SB_E_CUDA);
   } else {
@@ -1006,12 +993,16 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   const int tiles = c->N / c->W;
   for (int g = 2; g <= 8; g *= 2)
     if (g <= c->C && c->M % g == 0 && (int64_t)c->B * tiles * g <= 2 * 148) c->G = g;
+  if (const char* ge = getenv("SBPCG_K1_G")) {  // debugging override of the coil-group count
+    const int g = atoi(ge);
+    if (g >= 1 && g <= 8 && g <= c->C && c->M % g == 0) c->G = g;
+  }
   // algorithmic bytes per problem-launch of the matvec: coil maps
   // 8NC + z, p_{k-1}, x read + p_k, x, q written (6 x 8N) + the mask (4M floats for line
   // masks, one byte per plane pixel otherwise)
   c->k1_bytes = 8.0 * (double)img * c->C + 48.0 * (double)img +
                 (c->separable ? 4.0 * c->M : (double)(d3 ? (size_t)D1 * D2 : img));
-  sb_status s = c->separable ? make_tmap(c) : SB_OK;
+  sb_status s = c->plane ? SB_OK : make_tmap(c);  // K1 streams the coil maps by TMA
   if (s) {
     sb_pcg_destroy(c);
     return s;
