@@ -177,6 +177,27 @@ sb_status sb_set_kernel_timing(sb_ctx* ctx, int32_t enable);
 sb_status sb_get_kernel_time(sb_ctx* ctx, int32_t which /*0 = matvec K1, 1 = precond K2*/,
                              double* ms, int64_t* launches, double* alg_bytes_per_launch);
 
+/* ------------------------------------------------------------------------------------
+ * Coil-sharded mode (BASELINE config 5 over G GPUs).  One process per GPU; rank
+ * r creates its context with ITS coil shard (sens [B][C_r][...]) and the full mask, then
+ * attaches a communicator.  Every vector is replicated; per matvec each rank computes its
+ * partial coil sum sum_{c in r} S_c^H F^H R F S_c p and ONE NCCL all-reduce (sum, fp32) of
+ * that image forms the data term of A; the preconditioner, the regulariser,
+ * the dots and the SB steps then run identically on every rank (the all-reduce result is
+ * bitwise identical across ranks, so no scalar all-reduce is needed).  Lambda's coil
+ * marginal, u_1 and the RSS init are all-reduced as well.  The PCG loop is host-driven in
+ * this mode (no CUDA graph).  NCCL is loaded at run time (the process's libnccl.so.2, or
+ * SBPCG_NCCL_LIB).  Requires the plane path (ndim = 3, or a non-separable 2D mask).
+ * ------------------------------------------------------------------------------------ */
+typedef struct sb_comm sb_comm;
+/* rank 0: a 128-byte NCCL unique id to broadcast to the other ranks (out of band). */
+sb_status sb_comm_unique_id(void* id_out);
+/* Collective over the `world` ranks; binds to the current CUDA device.  SB_E_COMM on failure. */
+sb_status sb_comm_init(const void* id, int32_t rank, int32_t world, sb_comm** out);
+void sb_comm_destroy(sb_comm* comm);
+/* Attach (comm != NULL) or detach the communicator; rebuilds Lambda (collective). */
+sb_status sb_pcg_set_comm(sb_ctx* ctx, sb_comm* comm);
+
 /* Number of kernels launched by this context since creation (for bench.py). */
 int64_t sb_kernel_launch_count(const sb_ctx* ctx);
 

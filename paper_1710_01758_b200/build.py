@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libsbpcg.so")
-SOURCES = ["sbpcg.cu", "k_matvec.cu", "k_passes.cu", "k_lambda.cu", "k_sb.cu", "k_plane.cu", "k_plane3.cu"]
+SOURCES = ["sbpcg.cu", "k_matvec.cu", "k_passes.cu", "k_lambda.cu", "k_sb.cu", "k_plane.cu", "k_plane3.cu", "k_coil.cu"]
 HEADERS = ["fft_core.cuh", "internal.cuh", "kernels.cuh", "pcg_fin.cuh", "k_plane.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
@@ -52,7 +52,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 sys.stderr.write(log)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < _newest(objs):
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
-               *objs, "-o", LIB]
+               *objs, "-ldl", "-o", LIB]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

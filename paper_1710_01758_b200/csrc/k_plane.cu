@@ -70,7 +70,8 @@ __device__ __forceinline__ float2* peer(float2* p, int rank) {
 }
 
 template <int NY, int NZ, int G, int MODE>
-__global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T) kp_plane(const KPArgs a) {
+__global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T <= 256 ? 2 : 1)
+    kp_plane(const KPArgs a) {
   const bool D3 = a.d3 != 0;
   using P = PlaneCfg<NY, NZ, G>;
   constexpr int NYL = P::NYL, KB = P::KB, N1 = P::N1, N2 = P::N2, T = P::T;
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T) kp_plane(const KPArgs 
 
   for (int c = 0; c < ncoil; ++c) {
     const size_t soff = ((size_t)b * a.C + c) * img + (size_t)xpl * PN;
-    float2 s[N1], v[N1];
+    float2 v[N1];
     if constexpr (MODE != KP_ADJOINT) {
       // (1) row FFTs of s_c . p (or the preconditioner plane)
 #pragma unroll
@@ -215,8 +216,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T) kp_plane(const KPArgs 
         } else if constexpr (MODE == KP_PRE2D) {
           v[n1] = rk[n1];
         } else {
-          s[n1] = a.sens[soff + (size_t)(G * r + g) * NZ + z];
-          v[n1] = cmul(s[n1], pt[r * NZ + z]);
+          v[n1] = cmul(a.sens[soff + (size_t)(G * r + g) * NZ + z], pt[r * NZ + z]);
         }
       }
       fft_fwd<NZ, typename P::RLay>(v, wb, twz, j, r);
@@ -237,7 +237,6 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T) kp_plane(const KPArgs 
       }
     } else {
       // adjoint: the rows about to be overwritten by peers must be free (previous coil done)
-      (void)s;
     }
     cl_sync<G>();
     // (3) cross-cluster DFT, pointwise operator, inverse cross-cluster DFT
@@ -326,8 +325,9 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T) kp_plane(const KPArgs 
       }
     } else {
 #pragma unroll
-      for (int n1 = 0; n1 < N1; ++n1) {
-        const float2 t = cmulc(s[n1], v[n1]);
+      for (int n1 = 0; n1 < N1; ++n1) {  // s_c re-read (L2) rather than held across the transform
+        const float2 sv = a.sens[soff + (size_t)(G * r + g) * NZ + N2 * n1 + j];
+        const float2 t = cmulc(sv, v[n1]);
         acc[n1].x += t.x;
         acc[n1].y += t.y;
       }
@@ -340,7 +340,14 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T) kp_plane(const KPArgs 
     for (int n1 = 0; n1 < N1; ++n1) {
       const size_t gi = gidx(r, N2 * n1 + j);
       a.out[gi] = acc[n1];
-      if (a.out2 != nullptr) a.out2[gi] = make_float2(sqrtf(rss[n1]), 0.f);
+      if (a.out2 != nullptr) a.out2[gi] = make_float2(a.rss_raw ? rss[n1] : sqrtf(rss[n1]), 0.f);
+    }
+  }
+  if constexpr (MATVEC) {
+    if (a.acc_out != nullptr) {  // coil-sharded: partial coil sum out, epilogue after the all-reduce
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) a.acc_out[gidx(r, N2 * n1 + j)] = acc[n1];
+      return;
     }
   }
   if constexpr (MODE == KP_PRE2D) {

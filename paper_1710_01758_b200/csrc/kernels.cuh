@@ -156,9 +156,17 @@ struct KPArgs {
   float2* rout;
   float2* zout;
   int pmode;                 // -1 standalone apply, 0 PCG init, 1 PCG iteration
+  // coil-sharded mode: the matvec kernel stops after the coil loop and
+  // writes this rank's partial sum_c conj(s_c) F^H R F (s_c p) to acc_out; after the NCCL
+  // all-reduce the epilogue kernel (k_coil.cu) reads the reduced sum from acc_in.
+  float2* acc_out;
+  const float2* acc_in;
+  int rss_raw;               // ADJOINT: out2 = sum_c |.|^2 (no sqrt; all-reduced first)
   Loop L;
   Partials P;
 };
+cudaError_t launch_kc_epilogue(int mode, const KPArgs& a, cudaStream_t st);  // k_coil.cu
+cudaError_t launch_kc_sqrt_re(float2* v, size_t n, cudaStream_t st);
 
 // Programmatic dependent launch on/off for subsequent launches (host-side switch; the
 // graph builder turns it off while capturing unless SBPCG_GRAPH_PDL=1).

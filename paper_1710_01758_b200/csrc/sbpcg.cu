@@ -4,6 +4,7 @@
 // Method: PAPER.md:87-244 (see include/sbpcg.h for per-call citations).  PyTorch is not
 // used here; the Python binding passes raw pointers and a cudaStream_t.
 #include <cudaTypedefs.h>
+#include <dlfcn.h>
 
 #include <cstdlib>
 
@@ -28,6 +29,44 @@ static bool env_flag(const char* name, bool dflt) {
   if (!v) return dflt;
   return v[0] == '1';
 }
+
+// ------------------------------------------------------------------ NCCL (coil-sharded mode)
+// NCCL is resolved at run time (dlopen of the libnccl.so.2 the process already uses — the one
+// torch.distributed loaded — or SBPCG_NCCL_LIB), so the library has no link-time dependency.
+typedef struct { char internal[128]; } nccl_uid_t;
+typedef void* nccl_comm_t;
+enum { NCCL_SUM = 0, NCCL_FLOAT32 = 7, NCCL_FLOAT64 = 8 };
+struct NcclApi {
+  void* h = nullptr;
+  int (*getUniqueId)(nccl_uid_t*) = nullptr;
+  int (*commInitRank)(nccl_comm_t*, int, nccl_uid_t, int) = nullptr;
+  int (*commDestroy)(nccl_comm_t) = nullptr;
+  int (*allReduce)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+  const char* (*getErrorString)(int) = nullptr;
+};
+static NcclApi g_nccl;
+static bool nccl_load() {
+  if (g_nccl.allReduce) return true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) {
+    const char* e = getenv("SBPCG_NCCL_LIB");
+    h = dlopen(e ? e : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  }
+  if (!h) return false;
+  g_nccl.h = h;
+  g_nccl.getUniqueId = (int (*)(nccl_uid_t*))dlsym(h, "ncclGetUniqueId");
+  g_nccl.commInitRank = (int (*)(nccl_comm_t*, int, nccl_uid_t, int))dlsym(h, "ncclCommInitRank");
+  g_nccl.commDestroy = (int (*)(nccl_comm_t))dlsym(h, "ncclCommDestroy");
+  g_nccl.allReduce =
+      (int (*)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t))dlsym(h, "ncclAllReduce");
+  g_nccl.getErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+  return g_nccl.getUniqueId && g_nccl.commInitRank && g_nccl.commDestroy && g_nccl.allReduce;
+}
+
+struct sb_comm {
+  nccl_comm_t comm = nullptr;
+  int rank = 0, world = 1;
+};
 
 struct GraphSlot {
   cudaGraphExec_t exec = nullptr;
@@ -55,6 +94,8 @@ struct sb_ctx {
   double2 *twd_y = nullptr, *twd_z = nullptr;
   float2* bz[2] = {nullptr, nullptr};       // 3D TV auxiliary b_z
   double k1_bytes = 0;          // algorithmic bytes per problem-launch of the matvec
+  sb_comm* comm = nullptr;      // coil-sharded mode (this context holds a coil shard)
+  float2* accbuf = nullptr;     // [B][img] partial / all-reduced coil sum
   float mu = 0, lam = 0, gam = 0;
   bool separable = false;
   int W = 8, G = 1;
@@ -308,6 +349,26 @@ static void timing_collect(sb_ctx* c) {
   c->evnext = 0;
 }
 
+static sb_status allreduce(sb_ctx* c, void* buf, size_t count, int dtype, cudaStream_t st) {
+  const int r = g_nccl.allReduce(buf, buf, count, dtype, NCCL_SUM, c->comm->comm, st);
+  if (r != 0)
+    return fail(c, SB_E_COMM, std::string("ncclAllReduce: ") + (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "?"));
+  return SB_OK;
+}
+
+// Coil-sharded matvec: plane kernel up to the partial coil sum, all-reduce, epilogue.
+static sb_status run_kp_sharded(sb_ctx* c, int mode, KPArgs k, cudaStream_t st) {
+  k.acc_out = c->accbuf;
+  sb_status s = run_kp(c, mode, k, st);
+  if (s) return s;
+  if ((s = allreduce(c, c->accbuf, 2 * (size_t)c->B * c->img, NCCL_FLOAT32, st))) return s;
+  k.acc_out = nullptr;
+  k.acc_in = c->accbuf;
+  CK(launch_kc_epilogue(mode, k, st));
+  c->launches++;
+  return SB_OK;
+}
+
 // ------------------------------------------------------------------ kernel sequences
 // q = A v (generic or separable)
 static sb_status seq_apply(sb_ctx* c, const float2* v, float2* out, cudaStream_t st) {
@@ -315,7 +376,7 @@ static sb_status seq_apply(sb_ctx* c, const float2* v, float2* out, cudaStream_t
     KPArgs k = base_kp(c);
     k.vin = v;
     k.out = out;
-    return run_kp(c, KP_APPLY, k, st);
+    return c->comm ? run_kp_sharded(c, KP_APPLY, k, st) : run_kp(c, KP_APPLY, k, st);
   }
   K1Args a = base_k1(c);
   a.vin = v;
@@ -339,7 +400,7 @@ static sb_status seq_resid(sb_ctx* c, Loop L, const float2* bgiven, bool recon, 
     k.eps = eps;
     k.maxit = maxit;
     k.L = L;
-    return run_kp(c, KP_RESID, k, st);
+    return c->comm ? run_kp_sharded(c, KP_RESID, k, st) : run_kp(c, KP_RESID, k, st);
   }
   K1Args a = base_k1(c);
   a.vin = c->x;
@@ -406,7 +467,7 @@ static sb_status seq_body(sb_ctx* c, Loop L, int precond, cudaStream_t st, int* 
     KPArgs k = base_kp(c);
     k.out = c->q;
     k.L = L;
-    if ((s = run_kp(c, KP_PCG, k, st))) return s;
+    if ((s = c->comm ? run_kp_sharded(c, KP_PCG, k, st) : run_kp(c, KP_PCG, k, st))) return s;
     if ((s = seq_precond(c, L, precond, 1, c->r, c->z, st))) return s;
     if (nk) *nk = (int)c->launches - n0;
     return SB_OK;
@@ -478,8 +539,19 @@ static sb_status seq_adjoint3(sb_ctx* c, const float2* ydev, float2* xout, float
   k.tmp = c->tmpc;
   k.out = xout;
   k.out2 = rssout;
+  k.rss_raw = c->comm ? 1 : 0;
   k.scale = 1.0f / std::sqrt((float)c->img);
-  return run_kp(c, KP_ADJOINT, k, st);
+  if ((s = run_kp(c, KP_ADJOINT, k, st))) return s;
+  if (c->comm) {  // sum over all ranks' coils
+    const size_t n = (size_t)c->B * c->img;
+    if ((s = allreduce(c, xout, 2 * n, NCCL_FLOAT32, st))) return s;
+    if (rssout) {
+      if ((s = allreduce(c, rssout, 2 * n, NCCL_FLOAT32, st))) return s;
+      CK(launch_kc_sqrt_re(rssout, n, st));
+      c->launches++;
+    }
+  }
+  return SB_OK;
 }
 
 static sb_status seq_init_recon(sb_ctx* c, const float2* ydev, cudaStream_t st) {
@@ -620,7 +692,7 @@ static sb_status eager_solve(sb_ctx* c, int kind, const sb_pcg_opts* o, const fl
 }
 
 static sb_status run_solve_kind(sb_ctx* c, int kind, const sb_pcg_opts* o, const float2* ydev) {
-  if (o->use_graph && !c->timing) {
+  if (o->use_graph && !c->timing && !c->comm) {  // coil-sharded mode runs the host-driven loop
     sb_status s = build_graph(c, kind, o, ydev);
     if (s) return s;
     CK(cudaGraphLaunch(c->gs[kind].exec, c->st));
@@ -711,6 +783,10 @@ static sb_status build_lambda3(sb_ctx* c) {
       CK(launch_lambda_chunk(a, c->st));
       c->launches += 2;
     }
+  }
+  if (c->comm) {  // the marginal sums over ALL coils (every rank's shard)
+    sb_status s = allreduce(c, g, 2 * (size_t)c->B * pn, NCCL_FLOAT64, c->st);
+    if (s) return s;
   }
   a.B = c->B;
   a.C = 1;
@@ -815,7 +891,7 @@ void sb_pcg_destroy(sb_ctx* c) {
                   c->x, c->r, c->z, c->q, c->p0, c->p1, c->tmp, c->bvec, c->u, c->u1, c->rhs,
                   c->bx[0], c->bx[1], c->by[0], c->by[1], c->bw, c->tmpc, c->stage_in, c->stage_out,
                   c->scal, c->ctl, c->counters, c->P.p0, c->P.p1, c->P.cnt, c->hist, c->log_iters, c->log_relres,
-                  c->pmask, c->tw_y, c->tw_z, c->twd_y, c->twd_z, c->bz[0], c->bz[1]};
+                  c->pmask, c->tw_y, c->tw_z, c->twd_y, c->twd_z, c->bz[0], c->bz[1], c->accbuf};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->cap1) cudaStreamDestroy(c->cap1);
@@ -938,7 +1014,9 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
       sb_pcg_destroy(c);
       return SB_E_UNSUPPORTED_SIZE;
     }
-    c->pre2d = kp2_supported((int)M, (int)N) && env_flag("SBPCG_PRE2D", true);
+    // the fused one-kernel preconditioner (KP_PRE2D) is slower than the three column/row
+    // passes at the BASELINE sizes (measured: config 3 83k vs 135k it/s), so it is opt-in
+    c->pre2d = kp2_supported((int)M, (int)N) && env_flag("SBPCG_PRE2D", false);
     if (sep && cudaMemcpy(c->rowmask, rm.data(), rm.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(SB_E_CUDA);
   } else {
@@ -1014,6 +1092,48 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   }
   *out = c;
   return SB_OK;
+}
+
+sb_status sb_comm_unique_id(void* id_out) {
+  if (!id_out) return SB_E_ARG;
+  if (!nccl_load()) return SB_E_COMM;
+  nccl_uid_t id;
+  if (g_nccl.getUniqueId(&id) != 0) return SB_E_COMM;
+  memcpy(id_out, &id, sizeof(id));
+  return SB_OK;
+}
+
+sb_status sb_comm_init(const void* id, int32_t rank, int32_t world, sb_comm** out) {
+  if (!out || !id || world < 1 || rank < 0 || rank >= world) return SB_E_ARG;
+  *out = nullptr;
+  if (!nccl_load()) return SB_E_COMM;
+  nccl_uid_t uid;
+  memcpy(&uid, id, sizeof(uid));
+  sb_comm* cm = new sb_comm();
+  if (g_nccl.commInitRank(&cm->comm, world, uid, rank) != 0) {
+    delete cm;
+    return SB_E_COMM;
+  }
+  cm->rank = rank;
+  cm->world = world;
+  *out = cm;
+  return SB_OK;
+}
+
+void sb_comm_destroy(sb_comm* cm) {
+  if (!cm) return;
+  if (cm->comm && g_nccl.commDestroy) g_nccl.commDestroy(cm->comm);
+  delete cm;
+}
+
+sb_status sb_pcg_set_comm(sb_ctx* c, sb_comm* cm) {
+  sb_status s = check_ready(c);
+  if (s) return s;
+  if (!c->plane) return fail(c, SB_E_UNSUPPORTED_SIZE, "coil sharding needs the plane path (3D or non-separable 2D)");
+  if (cm && !c->accbuf) CK(dalloc(&c->accbuf, (size_t)c->B * c->img));
+  c->comm = cm;
+  for (auto& g : c->gs) g.maxit = -1;  // cached graphs do not apply
+  return build_lambda(c);               // Lambda from the marginal over all ranks' coils
 }
 
 sb_status sb_pcg_build_precond(sb_ctx* c) {

@@ -63,6 +63,10 @@ _sig = {
     "sb_get_kernel_time": (C.c_int, [_vp, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                      C.POINTER(C.c_double)]),
     "sb_kernel_launch_count": (C.c_int64, [_vp]),
+    "sb_comm_unique_id": (C.c_int, [_vp]),
+    "sb_comm_init": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(_vp)]),
+    "sb_comm_destroy": (None, [_vp]),
+    "sb_pcg_set_comm": (C.c_int, [_vp, _vp]),
     "sb_pcg_destroy": (None, [_vp]),
     "sb_status_str": (C.c_char_p, [C.c_int]),
     "sb_last_error": (C.c_char_p, [_vp]),
@@ -230,8 +234,57 @@ class SbPcg:
                     "kernel_time")
         return ms.value, n.value, by.value
 
+    def set_comm(self, comm: Optional["SbComm"]):
+        """Coil-sharded mode: this context holds one rank's coil shard; rebuilds Lambda from
+        the marginal over all ranks' coils (collective)."""
+        self._comm = comm
+        self._check(_lib.sb_pcg_set_comm(self._h, comm._h if comm is not None else None), "set_comm")
+
     def launches(self) -> int:
         return int(_lib.sb_kernel_launch_count(self._h))
+
+
+class SbComm:
+    """NCCL communicator of the coil-sharded mode (include/sbpcg.h "Coil-sharded mode").
+    The 128-byte unique id is created on rank 0 (`unique_id()`) and passed to every rank out of
+    band (e.g. torch.distributed.broadcast_object_list); construction is collective."""
+
+    def __init__(self, uid: bytes, rank: int, world: int):
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        buf = C.create_string_buffer(uid, 128)
+        h = _vp()
+        st = _lib.sb_comm_init(buf, int(rank), int(world), C.byref(h))
+        if st != 0:
+            raise SbError(st, "sb_comm_init failed")
+        self._h, self.rank, self.world = h, rank, world
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        st = _lib.sb_comm_unique_id(buf)
+        if st != 0:
+            raise SbError(st, "sb_comm_unique_id failed")
+        return buf.raw
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.sb_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def coil_shard(coils: int, rank: int, world: int):
+    """Contiguous coil range [c0, c1) of `rank` in the coil-sharded mode:
+    the first coils % world ranks take one extra coil."""
+    base, extra = divmod(coils, world)
+    c0 = rank * base + min(rank, extra)
+    return c0, c0 + base + (1 if rank < extra else 0)
 
 
 def abi_version() -> int:

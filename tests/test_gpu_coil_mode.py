@@ -1,0 +1,47 @@
+"""Coil-sharded mode (SURVEY 8(e), config 5 over G GPUs) on one GPU: a world-size-1 NCCL
+communicator exercises the whole sharded data path (plane kernel partial sum -> ncclAllReduce
+-> epilogue kernel, host-driven loop, all-reduced Lambda marginal / u_1 / RSS); results must
+equal the unsharded context.  The multi-rank decomposition itself is covered on CPU by
+tests/test_coil_shard_gloo.py."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import problems
+from tests.helpers import relerr
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_1710_01758_b200 import SbComm, SbPcg
+
+
+def _ctx(p, comm=None):
+    c = SbPcg(torch.from_numpy(p["sens"][None]).to(torch.complex64).cuda(),
+              torch.from_numpy(p["mask"][None]).cuda(), 1.0, 0.01, 0.01, 2)
+    if comm is not None:
+        c.set_comm(comm)
+    return c
+
+
+def test_coil_mode_world1_equals_unsharded():
+    p = synth.problem3d(5, shape=(8, 32, 32), coils=4, amplitude=100.0)
+    y = problems.make_kspace(p["phantom"], p["sens"], p["mask"], p["noise"])
+    comm = SbComm(SbComm.unique_id(), 0, 1)
+    a, b = _ctx(p), _ctx(p, comm)
+    np.testing.assert_allclose(a.get_k().numpy(), b.get_k().numpy(), rtol=1e-12)
+    rng = np.random.default_rng(3)
+    x = torch.from_numpy((rng.standard_normal((1, 8, 32, 32)) + 1j * rng.standard_normal((1, 8, 32, 32)))
+                         .astype(np.complex64)).cuda()
+    assert relerr(b.apply_A(x).cpu().numpy(), a.apply_A(x).cpu().numpy()) <= 1e-6
+    yt = torch.from_numpy(y[None]).to(torch.complex64).cuda()
+    xa, la = a.recon(yt, 3, eps=0.0, max_iters=6)
+    xb, lb = b.recon(yt, 3, eps=0.0, max_iters=6)
+    assert la["pcg_iters"] == lb["pcg_iters"]
+    assert relerr(xb.cpu().numpy(), xa.cpu().numpy()) <= 1e-5
+    xa, la = a.recon(yt, 3, eps=1e-4, max_iters=40)
+    xb, lb = b.recon(yt, 3, eps=1e-4, max_iters=40)
+    assert la["pcg_iters"] == lb["pcg_iters"]
+    assert relerr(xb.cpu().numpy(), xa.cpu().numpy()) <= 1e-5
+    a.close(), b.close(), comm.close()
