@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--precond", type=int, default=1)
+    ap.add_argument("--precond", type=int, default=1, choices=[0, 1, 2], help="0 none, 1 circulant, 2 Jacobi")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -183,7 +183,7 @@ def run_reference(args):
         t = time.perf_counter()
         x, log = sb.sb_recon(y, p["sens"], p["mask"], prm.mu, prm.lam, prm.gamma, 1, 1,
                              prm.wavelet_levels, prm.eps, prm.max_iters,
-                             "circulant" if args.precond else "none")
+                             ["none", "circulant", "jacobi"][args.precond])
         return time.perf_counter() - t, sum(log.pcg_iters)
 
     for _ in range(args.warmup):
@@ -266,7 +266,7 @@ def cpu_baseline_sample(cfg, precond):
     n_outer = 2
     t = time.perf_counter()
     _, log = sb.sb_recon(y, p["sens"], p["mask"], prm.mu, prm.lam, prm.gamma, n_outer, 1,
-                         prm.wavelet_levels, prm.eps, prm.max_iters, "circulant" if precond else "none")
+                         prm.wavelet_levels, prm.eps, prm.max_iters, ["none", "circulant", "jacobi"][precond])
     dt = time.perf_counter() - t
     it = sum(log.pcg_iters)
     return {"value": it / dt, "unit": "PCG iters/s", "cores": 1, "kind": "oracle",
@@ -453,7 +453,7 @@ def run_ours(args):
                        "coils": spec.coils, "mask": mask_desc,
                        "mu": prm.mu, "lambda": prm.lam, "gamma": prm.gamma, "n_outer": prm.n_outer,
                        "pcg_eps": prm.eps, "pcg_max_iters": prm.max_iters,
-                       "precond": "circulant" if args.precond else "none",
+                       "precond": ["none", "circulant", "jacobi"][args.precond],
                        "pcg_iters_per_step": it_sum / args.steps / (1 if coil_mode else ws),
                        "parallelism": (f"coil-sharded x{ws} (NCCL all-reduce per matvec)" if coil_mode
                                        else (f"slice-sharded x{ws}" if ws > 1 else "1 GPU")),

@@ -116,7 +116,9 @@ sb_status sb_adjoint(sb_ctx* ctx, const sb_c64* y, sb_c64* x);
 typedef struct {
   float eps;          /* stop when ||r_k||/||b|| <= eps; 0 => fixed count   */
   int32_t max_iters;  /* >= 1                                                              */
-  int32_t precond;    /* 0 none, 1 circulant                                */
+  int32_t precond;    /* 0 none, 1 circulant, 2 Jacobi z = r/diag(A) with  */
+                      /* diag(A) = mu f sum_c |S_c|^2 + 2 nd lambda + gamma (PAPER.md:187;  */
+                      /* f = sampled fraction; built on first use)                         */
   int32_t use_graph;  /* 1: device-driven loop in a CUDA graph (conditional while node)   */
 } sb_pcg_opts;
 

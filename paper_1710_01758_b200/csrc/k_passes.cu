@@ -9,6 +9,8 @@
 // Column passes: one CTA = W columns x all M rows of one image, threads (j, col) with col
 // fastest (coalesced rows of W*8 bytes).  Row passes: one CTA = LINES rows, threads
 // (line, j) with j fastest.  Each transform is the four-step register FFT of fft_core.cuh.
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "pcg_fin.cuh"
 
@@ -286,7 +288,8 @@ __global__ void __launch_bounds__(RowCfg<N, LINES_>::NT) k_row(const PassArgs a)
 }
 
 // ------------------------------------------------------------------ elementwise kernels
-// No preconditioner (precond = 0): r -= alpha q (PCG), z = r, rho' = ||r||^2.
+// No preconditioner (precond = 0): r -= alpha q (PCG), z = r, rho' = ||r||^2; or the Jacobi
+// preconditioner (precond = 2; jinv = 1/diag(A)): z = jinv . r, rho' = <r, z>.
 __global__ void __launch_bounds__(256) k_nopre(const PassArgs a) {
   __shared__ double red[32];
   __shared__ int lastflag;
@@ -299,16 +302,19 @@ __global__ void __launch_bounds__(256) k_nopre(const PassArgs a) {
     return;
   }
   const double alpha = (a.mode == 1) ? a.L.scal[b].alpha : 0.0;
-  double d0 = 0.0;
+  const float* ji = a.jinv != nullptr ? a.jinv + (size_t)b * img : nullptr;
+  double d0 = 0.0, d1 = 0.0;  // ||r||^2, <r, z>
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < img; i0 += 4 * stride) {
     float2 r[4], q[4];
+    float w[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const size_t i = i0 + u * stride;
       if (i < img) {
         r[u] = a.a0[(size_t)b * img + i];
         q[u] = (a.mode == 1) ? a.a1[(size_t)b * img + i] : make_float2(0.f, 0.f);
+        w[u] = ji != nullptr ? ji[i] : 1.f;
       }
     }
 #pragma unroll
@@ -321,27 +327,51 @@ __global__ void __launch_bounds__(256) k_nopre(const PassArgs a) {
         r[u].y -= (float)alpha * q[u].y;
         a.o0[gi] = r[u];
       }
-      a.o1[gi] = r[u];  // z = r
+      const float2 z = make_float2(w[u] * r[u].x, w[u] * r[u].y);
+      a.o1[gi] = z;
       d0 += (double)r[u].x * r[u].x + (double)r[u].y * r[u].y;
+      d1 += (double)r[u].x * z.x + (double)r[u].y * z.y;
     }
   }
   const double s0 = block_sum(d0, red);
+  const double s1 = block_sum(d1, red);
   const int nblk = gridDim.x;
-  if (publish_and_check_last(s0, 0.0, a.P, b, blockIdx.x, nblk, &lastflag)) {
+  if (publish_and_check_last(s0, s1, a.P, b, blockIdx.x, nblk, &lastflag)) {
     if (threadIdx.x < 32) {
-      const double t = warp_sum_partials(a.P.p0 + (size_t)b * a.P.cap, nblk);
+      const double trr = warp_sum_partials(a.P.p0 + (size_t)b * a.P.cap, nblk);
+      const double trz = warp_sum_partials(a.P.p1 + (size_t)b * a.P.cap, nblk);
       if (threadIdx.x == 0) {
         if (a.mode == 1) {
-          fin_rr(a.L, b, t);
-          if (a.L.scal[b].active) fin_rho(a.L, b, t, false);
+          fin_rr(a.L, b, trr);
+          if (a.L.scal[b].active) fin_rho(a.L, b, trz, false);
         } else {
-          fin_rho(a.L, b, t, true);
+          fin_rho(a.L, b, trz, true);
         }
         a.P.cnt[b] = 0;
         slice_arrive(a.L);
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(256) k_jacobi_diag(const float2* sens, const float* frac, int C, size_t img,
+                                                     float cst, float mu, float* jinv) {
+  const int b = blockIdx.y;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < img; i += (size_t)gridDim.x * blockDim.x) {
+    float s2 = 0.f;
+    for (int c = 0; c < C; ++c) {
+      const float2 v = sens[((size_t)b * C + c) * img + i];
+      s2 += v.x * v.x + v.y * v.y;
+    }
+    jinv[(size_t)b * img + i] = 1.f / (mu * frac[b] * s2 + cst);
+  }
+}
+
+cudaError_t launch_jacobi_diag(const float2* sens, const float* frac, int B, int C, size_t img, int nd, float mu,
+                               float lam, float gam, float* jinv, cudaStream_t st) {
+  const int nb = (int)std::min<size_t>(1024, (img + 255) / 256);
+  k_jacobi_diag<<<dim3(nb, B), 256, 0, st>>>(sens, frac, C, img, 2.f * nd * lam + gam, mu, jinv);
+  return cudaGetLastError();
 }
 
 // PCG exit: x += alpha_K p_K (the last completed iteration), or x = 0 when ||b|| = 0.

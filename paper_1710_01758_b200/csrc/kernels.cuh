@@ -64,6 +64,8 @@ struct PassArgs {
   float2* pbuf0;
   float2* pbuf1;
   float2* x;
+  // Jacobi preconditioner: z = r . jinv, jinv = 1/diag(A) [B][N]
+  const float* jinv;
 };
 
 // fp64 Lambda build (k_lambda.cu)
@@ -221,6 +223,9 @@ enum PassKind {
   P_COL_INV = 12,        // o0[b][c] = colIFFT(a0[b][c]) * scale  (3D: the d0 transform of E^H)
 };
 cudaError_t launch_pass(int kind, const PassArgs& a, cudaStream_t st);
+// jinv[b][i] = 1 / (mu f_b sum_c |s_c(i)|^2 + 2 nd lambda + gamma)
+cudaError_t launch_jacobi_diag(const float2* sens, const float* frac, int B, int C, size_t img, int nd, float mu,
+                               float lam, float gam, float* jinv, cudaStream_t st);
 bool pass_supported(int M, int N);
 
 cudaError_t launch_kp2(int mode, const KPArgs& a, cudaStream_t st);  // 2D, matvec modes

@@ -96,6 +96,8 @@ struct sb_ctx {
   double k1_bytes = 0;          // algorithmic bytes per problem-launch of the matvec
   sb_comm* comm = nullptr;      // coil-sharded mode (this context holds a coil shard)
   float2* accbuf = nullptr;     // [B][img] partial / all-reduced coil sum
+  float* jinv = nullptr;        // Jacobi: 1/diag(A) [B][img] (built on first use)
+  std::vector<float> samp_frac; // sampled fraction f of each problem's mask
   float mu = 0, lam = 0, gam = 0;
   bool separable = false;
   int W = 8, G = 1;
@@ -425,11 +427,12 @@ static sb_status seq_precond(sb_ctx* c, Loop L, int precond, int mode, const flo
   pa.L = L;
   pa.mode = mode;
   sb_status s;
-  if (precond == 0) {
+  if (precond == 0 || precond == 2) {  // none, or Jacobi z = r / diag(A)
     pa.a0 = c->r;
     pa.a1 = c->q;
     pa.o0 = c->r;
     pa.o1 = c->z;
+    pa.jinv = precond == 2 ? c->jinv : nullptr;
     return run_pass(c, P_NOPRE, pa, st);
   }
   if (c->pre2d) {  // one cluster kernel: r -= alpha q, ||r||^2, z = F^H Lambda^{-1} F r, <r, z>
@@ -891,7 +894,7 @@ void sb_pcg_destroy(sb_ctx* c) {
                   c->x, c->r, c->z, c->q, c->p0, c->p1, c->tmp, c->bvec, c->u, c->u1, c->rhs,
                   c->bx[0], c->bx[1], c->by[0], c->by[1], c->bw, c->tmpc, c->stage_in, c->stage_out,
                   c->scal, c->ctl, c->counters, c->P.p0, c->P.p1, c->P.cnt, c->hist, c->log_iters, c->log_relres,
-                  c->pmask, c->tw_y, c->tw_z, c->twd_y, c->twd_z, c->bz[0], c->bz[1], c->accbuf};
+                  c->pmask, c->tw_y, c->tw_z, c->twd_y, c->twd_z, c->bz[0], c->bz[1], c->accbuf, c->jinv};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->cap1) cudaStreamDestroy(c->cap1);
@@ -993,6 +996,13 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   for (uint8_t v : hm)
     if (v > 1) return bail(SB_E_ARG);
   const int nm = c->mask_shared ? 1 : c->B;
+  c->samp_frac.assign(c->B, 0.f);
+  for (int b = 0; b < c->B; ++b) {
+    const uint8_t* mb = hm.data() + (size_t)(c->mask_shared ? 0 : b) * img;
+    size_t cnt = 0;
+    for (size_t i = 0; i < img; ++i) cnt += mb[i];
+    c->samp_frac[b] = (float)((double)cnt / (double)img);
+  }
   if (!d3) {
     // separability (rows constant along d1): the line-mask identity of K1 (DESIGN.md a1)
     bool sep = true;
@@ -1247,8 +1257,18 @@ sb_status sb_adjoint(sb_ctx* c, const sb_c64* y, sb_c64* x) {
 }
 
 static sb_status check_opts(sb_ctx* c, const sb_pcg_opts* o) {
-  if (!o || o->max_iters < 1 || !(o->eps >= 0.f) || (o->precond != 0 && o->precond != 1))
+  if (!o || o->max_iters < 1 || !(o->eps >= 0.f) || o->precond < 0 || o->precond > 2)
     return fail(c, SB_E_ARG, "bad pcg options");
+  if (o->precond == 2 && !c->jinv) {  // Jacobi diagonal, once
+    CK(dalloc(&c->jinv, (size_t)c->B * c->img));
+    float* fr = nullptr;
+    CK(dalloc(&fr, c->B));
+    CK(cudaMemcpy(fr, c->samp_frac.data(), c->B * sizeof(float), cudaMemcpyHostToDevice));
+    CK(launch_jacobi_diag(c->sens, fr, c->B, c->C, c->img, c->ndim, c->mu, c->lam, c->gam, c->jinv, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    cudaFree(fr);
+    c->launches++;
+  }
   return SB_OK;
 }
 

@@ -105,7 +105,7 @@ def test_3d_encode_adjoint(case):
     ctx.close()
 
 
-@pytest.mark.parametrize("precond_kind", [1, 0])
+@pytest.mark.parametrize("precond_kind", [1, 0, 2])
 def test_3d_pcg_fixed_count(precond_kind):
     shape, coils, L = CASES3[0]
     ps = _prob3(shape, coils, B=2)
@@ -121,9 +121,12 @@ def test_3d_pcg_fixed_count(precond_kind):
         s32 = _c32(p["sens"])
         A = lambda v: ops.apply_A(v, s32, p["mask"], mu, lam, gam)  # noqa: E731
         Minv = None
-        if precond_kind:
+        if precond_kind == 1:
             k = precond.build_k(s32, p["mask"], mu, lam, gam)
             Minv = lambda v: precond.apply_Minv(v, k)  # noqa: E731
+        elif precond_kind == 2:
+            dj = precond.jacobi_diag(s32, p["mask"], mu, lam, gam)
+            Minv = lambda v: v / dj  # noqa: E731
         ref = pcg(A, _c32(bvec[b]), _c32(x0[b]), Minv, 0.0, 10)
         assert relerr(xg[b], ref.x) <= 1e-3, relerr(xg[b], ref.x)
         np.testing.assert_allclose(st["relres_hist"][b][:11], ref.relres, rtol=2e-2, atol=1e-6)

@@ -94,7 +94,7 @@ def test_encode_adjoint(case):
     ctx.close()
 
 
-@pytest.mark.parametrize("precond_kind", [1, 0])
+@pytest.mark.parametrize("precond_kind", [1, 0, 2])
 @pytest.mark.parametrize("use_graph", [True, False])
 def test_pcg_fixed_count_parity(precond_kind, use_graph):
     ps = batch(1, 3, (64, 64), 4)
@@ -111,9 +111,12 @@ def test_pcg_fixed_count_parity(precond_kind, use_graph):
         s32 = p["sens"].astype(np.complex64).astype(np.complex128)
         A = lambda v: ops.apply_A(v, s32, p["mask"], mu, lam, gam)  # noqa: E731
         Minv = None
-        if precond_kind:
+        if precond_kind == 1:
             k = precond.build_k(s32, p["mask"], mu, lam, gam)
             Minv = lambda v: precond.apply_Minv(v, k)  # noqa: E731
+        elif precond_kind == 2:  # Jacobi
+            dj = precond.jacobi_diag(s32, p["mask"], mu, lam, gam)
+            Minv = lambda v: v / dj  # noqa: E731
         ref = pcg(A, bvec[b].astype(np.complex64).astype(np.complex128),
                   x0[b].astype(np.complex64).astype(np.complex128), Minv, 0.0, 15)
         assert relerr(xg[b], ref.x) <= 1e-3
@@ -214,7 +217,7 @@ def test_sb_update_parity():
     ctx.close()
 
 
-@pytest.mark.parametrize("precond_kind", [1, 0])
+@pytest.mark.parametrize("precond_kind", [1, 0, 2])
 @pytest.mark.parametrize("amp", [1.0, 100.0])
 def test_sb_recon_config1_fixed_counts(precond_kind, amp):
     # BASELINE config 1: 64x64, 4 coils, TV + 1-level Haar, mu=1, lam=gam=0.05, 5 outer, CG 15
@@ -228,7 +231,7 @@ def test_sb_recon_config1_fixed_counts(precond_kind, amp):
     for b, p in enumerate(ps):
         s32 = p["sens"].astype(np.complex64).astype(np.complex128)
         ref, rlog = sb.sb_recon(p["y"].astype(np.complex64).astype(np.complex128), s32, p["mask"], mu, lam, gam,
-                                5, 1, 1, 0.0, 15, "circulant" if precond_kind else "none")
+                                5, 1, 1, 0.0, 15, ["none", "circulant", "jacobi"][precond_kind])
         assert relerr(xg[b], ref) <= 1e-3, relerr(xg[b], ref)
     ctx.close()
 
