@@ -346,6 +346,7 @@ def run_ours(args):
     st = torch.cuda.current_stream()
     total_ms = 0.0
     iters = 0
+    step_ms = []
     l0 = ctx.launches()
     for _ in range(args.steps):
         flush.fill_(1.0)  # L2 flush between timed steps (inputs < L2 at config 2)
@@ -355,7 +356,8 @@ def run_ours(args):
         log = step()
         e1.record(st)
         e1.synchronize()
-        total_ms += e0.elapsed_time(e1)
+        step_ms.append(e0.elapsed_time(e1))
+        total_ms += step_ms[-1]
         iters += sum(sum(r) for r in log["pcg_iters"])
     torch.cuda.synchronize()
     launches = ctx.launches() - l0
@@ -457,7 +459,8 @@ def run_ours(args):
                        "pcg_iters_per_step": it_sum / args.steps / (1 if coil_mode else ws),
                        "parallelism": (f"coil-sharded x{ws} (NCCL all-reduce per matvec)" if coil_mode
                                        else (f"slice-sharded x{ws}" if ws > 1 else "1 GPU")),
-                       "sb_recon_ms": ms_per_step, "l2": "flushed between timed steps (256 MiB write)",
+                       "sb_recon_ms": ms_per_step, "step_ms": [round(t, 3) for t in step_ms],
+                       "l2": "flushed between timed steps (256 MiB write)",
                        "loop": "CUDA graph, conditional while node" if use_graph else "eager"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,

@@ -48,8 +48,19 @@ struct PlaneCfg {
   static_assert(NYL <= 32, "column DFT is register resident");
   using RLay = typename RowLayout<NZ, NYL>::L;
   static constexpr int WBS = RowLayout<NZ, NYL>::size > NYL * NZ ? RowLayout<NZ, NYL>::size : NYL * NZ;
-  static constexpr size_t smem = (size_t)(WBS + NYL * NZ + NZ + NY) * sizeof(float2);
+  static constexpr size_t smem0 = (size_t)(WBS + NYL * NZ + NZ + NY) * sizeof(float2);
+  // prefetch buffer for the next coil's s_c tile (cp.async) when it does not cost occupancy:
+  // keep 2 CTAs/SM where they fit, else (already 1 CTA/SM) stay under the 227 KB limit
+  static constexpr size_t sbytes = (size_t)NYL * NZ * sizeof(float2);
+  static constexpr bool PREF = (smem0 + sbytes <= 110 * 1024) || (smem0 > 113 * 1024 && smem0 + sbytes <= 220 * 1024);
+  static constexpr size_t smem = smem0 + (PREF ? sbytes : 0);
 };
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 template <int G>
 __device__ __forceinline__ void cl_sync() {
@@ -70,7 +81,7 @@ __device__ __forceinline__ float2* peer(float2* p, int rank) {
 }
 
 template <int NY, int NZ, int G, int MODE>
-__global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T <= 256 ? 2 : 1)
+__global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T <= 128 ? 3 : (PlaneCfg<NY, NZ, G>::T <= 256 ? 2 : 1))
     kp_plane(const KPArgs a) {
   const bool D3 = a.d3 != 0;
   using P = PlaneCfg<NY, NZ, G>;
@@ -82,6 +93,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
   float2* pt = wb + P::WBS;                          // NYL x NZ: p (or x) tile, natural
   float2* twz = pt + NYL * NZ;                       // NZ
   float2* twy = twz + NZ;                            // NY
+  float2* sbuf = twy + NY;                           // P::PREF: next coil's s_c tile (NYL x NZ)
   __shared__ double red[32];
   __shared__ int lastflag;
 
@@ -202,6 +214,26 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
   }
   const uint8_t* mk = a.mask + (size_t)b * a.mask_bstride;
   float2 colv[NYL];
+  // the mask values this thread applies in stage (3): rows kb + NYL*ka, kb in this CTA's
+  // range, column kz = tid -> NYL <= 32 bits, loaded once
+  uint32_t mbits = 0;
+  if (tid < NZ) {
+#pragma unroll
+    for (int kbl = 0; kbl < KB; ++kbl)
+#pragma unroll
+      for (int ka = 0; ka < G; ++ka)
+        if (mk[(size_t)(g * KB + kbl + NYL * ka) * NZ + tid]) mbits |= 1u << (kbl * G + ka);
+  }
+  constexpr bool PF = P::PREF && (MATVEC || MODE == KP_ENCODE);
+  auto prefetch_s = [&](int cc) {  // s_cc tile (this CTA's rows) -> sbuf, 16-byte cp.async
+    const size_t so = ((size_t)b * a.C + cc) * img + (size_t)xpl * PN;
+    for (int e = tid; e < NYL * NZ / 2; e += T) {
+      const int row = e / (NZ / 2), c2 = e % (NZ / 2);
+      cp_async16(sbuf + row * NZ + 2 * c2, a.sens + so + (size_t)(G * row + g) * NZ + 2 * c2);
+    }
+    cp_async_commit();
+  };
+  if constexpr (PF) prefetch_s(0);
 
   for (int c = 0; c < ncoil; ++c) {
     const size_t soff = ((size_t)b * a.C + c) * img + (size_t)xpl * PN;
@@ -215,11 +247,20 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
           v[n1] = a.tmp[gidx(r, z)];
         } else if constexpr (MODE == KP_PRE2D) {
           v[n1] = rk[n1];
+        } else if constexpr (PF) {
+          if (n1 == 0) {
+            cp_async_wait_all();
+            __syncthreads();
+          }
+          v[n1] = cmul(sbuf[r * NZ + z], pt[r * NZ + z]);
         } else {
           v[n1] = cmul(a.sens[soff + (size_t)(G * r + g) * NZ + z], pt[r * NZ + z]);
         }
       }
       fft_fwd<NZ, typename P::RLay>(v, wb, twz, j, r);
+      if constexpr (PF) {  // every thread read sbuf before the barrier inside fft_fwd
+        if (c + 1 < ncoil) prefetch_s(c + 1);
+      }
       __syncthreads();
 #pragma unroll
       for (int q = 0; q < N1; ++q) wb[r * NZ + specidx<NZ>(j, q)] = v[q];
@@ -251,7 +292,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
           for (int ka = 0; ka < G; ++ka) {
             const int ky = kb + NYL * ka;
             const float2 yv = a.tmp[soff + (size_t)ky * NZ + kz];
-            const float f = mk[ky * NZ + kz] ? a.scale : 0.f;
+            const float f = ((mbits >> (kbl * G + ka)) & 1u) ? a.scale : 0.f;
             w[ka] = make_float2(yv.x * f, yv.y * f);
           }
         } else {
@@ -265,9 +306,9 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
             if constexpr (MODE == KP_PRECOND || MODE == KP_PRE2D) {
               f = a.lam_inv[boff + (size_t)xpl * PN + (size_t)ky * NZ + kz];
             } else if constexpr (MODE == KP_ENCODE) {
-              f = (a.full || mk[ky * NZ + kz]) ? a.scale : 0.f;
+              f = (a.full || ((mbits >> (kbl * G + ka)) & 1u)) ? a.scale : 0.f;
             } else {
-              f = mk[ky * NZ + kz] ? a.scale : 0.f;
+              f = ((mbits >> (kbl * G + ka)) & 1u) ? a.scale : 0.f;
             }
             w[ka] = make_float2(w[ka].x * f, w[ka].y * f);
           }
@@ -489,13 +530,19 @@ static cudaError_t kp_launch(const KPArgs& a, cudaStream_t st) {
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::smem);
     if (e != cudaSuccess) return e;
+    if (G > 8 && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+      return e;
     attr_done = true;
   }
   return launch_ex(kern, dim3(G, a.planes, a.B), dim3(P::T), P::smem, st, G > 1 ? G : 0, a);
 }
 
 // cluster size per plane height: the column DFT holds NY/G <= 32 values and G | NY/G
-template <int NY> struct PlaneG { static constexpr int value = NY <= 32 ? 1 : (NY <= 64 ? 2 : (NY <= 128 ? 4 : 8)); };
+// NY = 256 takes a 16-CTA (non-portable) cluster: 16 rows per CTA, every thread busy in
+// both the row and the column stage, no register spills (G = 8 spilled at 128 registers)
+template <int NY> struct PlaneG {
+  static constexpr int value = NY <= 32 ? 1 : (NY <= 64 ? 2 : (NY <= 128 ? 4 : (NY == 256 ? 16 : 8)));
+};
 
 template <int NY, int NZ>
 static cudaError_t kp_matvec_modes(int mode, const KPArgs& a, cudaStream_t st) {

@@ -72,7 +72,8 @@ struct GraphSlot {
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
   int nfixed = 0;      // kernels outside the loop
-  int nbody = 0;       // kernels per loop iteration
+  int nbody = 0;       // kernels per while-body (unroll iterations)
+  int unroll = 1;
   float eps = -1.f;
   int maxit = -1;
   int precond = -1;
@@ -98,6 +99,8 @@ struct sb_ctx {
   float2* accbuf = nullptr;     // [B][img] partial / all-reduced coil sum
   float* jinv = nullptr;        // Jacobi: 1/diag(A) [B][img] (built on first use)
   std::vector<float> samp_frac; // sampled fraction f of each problem's mask
+  void* lscr[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // Lambda build scratch (kept)
+  size_t lscr_bytes[5] = {0, 0, 0, 0, 0};
   float mu = 0, lam = 0, gam = 0;
   bool separable = false;
   int W = 8, G = 1;
@@ -639,7 +642,11 @@ static sb_status build_graph(sb_ctx* c, int kind, const sb_pcg_opts* o, const fl
   const int64_t lb = c->launches;
   CK(cudaStreamBeginCaptureToGraph(c->cap2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   int nk = 0;
-  s = seq_body(c, L, o->precond, c->cap2, &nk);
+  // U iterations per evaluation of the while condition (SBPCG_UNROLL, default 1): a problem
+  // that converges inside the group is frozen, so the extra kernels exit at once
+  const int U = std::max(1, std::min(8, getenv("SBPCG_UNROLL") ? atoi(getenv("SBPCG_UNROLL")) : 1));
+  for (int u = 0; u < U && !s; ++u) s = seq_body(c, L, o->precond, c->cap2, &nk);
+  g.unroll = U;
   cudaGraph_t bodyout;
   cudaError_t e2 = cudaStreamEndCapture(c->cap2, &bodyout);
   if (s || e2 != cudaSuccess) {
@@ -708,6 +715,23 @@ static sb_status run_solve_kind(sb_ctx* c, int kind, const sb_pcg_opts* o, const
 static sb_status build_lambda3(sb_ctx* c);
 static sb_status finish_lambda(sb_ctx* c, void* tmp, void* g, void* rh, int* bad, void* kc2);
 
+// Persistent Lambda-build scratch (allocated on the first build, reused by every rebuild so
+// that sb_pcg_build_precond does no cudaMalloc/cudaFree: those block the host).
+template <typename T>
+static cudaError_t lscratch(sb_ctx* c, int slot, T** p, size_t n) {
+  const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+  if (c->lscr_bytes[slot] < bytes) {
+    if (c->lscr[slot]) cudaFree(c->lscr[slot]);
+    c->lscr[slot] = nullptr;
+    c->lscr_bytes[slot] = 0;
+    cudaError_t e = cudaMalloc(&c->lscr[slot], bytes);
+    if (e != cudaSuccess) return e;
+    c->lscr_bytes[slot] = bytes;
+  }
+  *p = (T*)c->lscr[slot];
+  return cudaSuccess;
+}
+
 static sb_status build_lambda(sb_ctx* c) {
   if (c->ndim == 3) return build_lambda3(c);
   LamArgs a;
@@ -730,10 +754,10 @@ static sb_status build_lambda(sb_ctx* c) {
   a.tw_n = c->twd_n;
   double2 *tmp = nullptr, *g = nullptr, *rh = nullptr;
   int* bad = nullptr;
-  CK(dalloc(&tmp, (size_t)c->B * c->C * c->img));
-  CK(dalloc(&g, (size_t)c->B * c->img));
-  CK(dalloc(&rh, (size_t)a.nmask * c->img));
-  CK(dalloc(&bad, 1));
+  CK(lscratch(c, 0, &tmp, (size_t)c->B * c->C * c->img));
+  CK(lscratch(c, 1, &g, (size_t)c->B * c->img));
+  CK(lscratch(c, 2, &rh, (size_t)a.nmask * c->img));
+  CK(lscratch(c, 3, &bad, 1));
   CK(cudaMemsetAsync(bad, 0, sizeof(int), c->st));
   a.tmp = tmp;
   a.g = g;
@@ -767,11 +791,11 @@ static sb_status build_lambda3(sb_ctx* c) {
   double2 *tmp = nullptr, *g = nullptr, *rh = nullptr;
   double* kc2 = nullptr;
   int* bad = nullptr;
-  CK(dalloc(&tmp, (size_t)chunk * pn));
-  CK(dalloc(&g, (size_t)c->B * pn));
-  CK(dalloc(&rh, (size_t)a.nmask * pn));
-  CK(dalloc(&kc2, (size_t)c->B * pn));
-  CK(dalloc(&bad, 1));
+  CK(lscratch(c, 0, &tmp, (size_t)chunk * pn));
+  CK(lscratch(c, 1, &g, (size_t)c->B * pn));
+  CK(lscratch(c, 2, &rh, (size_t)a.nmask * pn));
+  CK(lscratch(c, 4, &kc2, (size_t)c->B * pn));
+  CK(lscratch(c, 3, &bad, 1));
   CK(cudaMemsetAsync(bad, 0, sizeof(int), c->st));
   a.tmp = tmp;
   a.rhat = rh;
@@ -820,11 +844,7 @@ static sb_status finish_lambda(sb_ctx* c, void* tmp, void* g, void* rh, int* bad
   int hb = 0;
   CK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
-  cudaFree(tmp);
-  cudaFree(g);
-  cudaFree(rh);
-  cudaFree(bad);
-  if (kc2) cudaFree(kc2);
+  (void)tmp, (void)g, (void)rh, (void)kc2;  // persistent scratch (lscratch)
   if (hb) return fail(c, SB_E_SINGULAR_K, "singular k (min |k| <= 1e-14 or non-finite)");
   return SB_OK;
 }
@@ -896,6 +916,8 @@ void sb_pcg_destroy(sb_ctx* c) {
                   c->scal, c->ctl, c->counters, c->P.p0, c->P.p1, c->P.cnt, c->hist, c->log_iters, c->log_relres,
                   c->pmask, c->tw_y, c->tw_z, c->twd_y, c->twd_z, c->bz[0], c->bz[1], c->accbuf, c->jinv};
   for (void* p : bufs)
+    if (p) cudaFree(p);
+  for (void* p : c->lscr)
     if (p) cudaFree(p);
   if (c->cap1) cudaStreamDestroy(c->cap1);
   if (c->cap2) cudaStreamDestroy(c->cap2);
@@ -1313,7 +1335,8 @@ sb_status sb_pcg_solve(sb_ctx* c, const sb_c64* b, sb_c64* x, const sb_pcg_opts*
   if (o->use_graph && !c->timing) {
     int mx = 0;
     for (auto& h : hs) mx = std::max(mx, h.iter);
-    c->launches += c->gs[0].nfixed + (int64_t)c->gs[0].nbody * mx;
+    const GraphSlot& g0 = c->gs[0];
+    c->launches += g0.nfixed + (int64_t)g0.nbody * ((mx + g0.unroll - 1) / g0.unroll);
   }
   if (stats) {
     std::vector<float> hist;
@@ -1383,7 +1406,7 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
       int mx = 0;
       for (int b = 0; b < c->B; ++b) mx = std::max(mx, li[(size_t)j * c->B + b]);
       const GraphSlot& g = c->gs[j == 0 ? 1 : 2 + ((j - 1) & 1)];
-      c->launches += g.nfixed + (int64_t)g.nbody * mx;
+      c->launches += g.nfixed + (int64_t)g.nbody * ((mx + g.unroll - 1) / g.unroll);
     }
   }
   if (log) {
