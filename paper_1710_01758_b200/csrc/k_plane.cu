@@ -51,7 +51,8 @@ struct PlaneCfg {
   static constexpr size_t smem0 = (size_t)(WBS + NYL * NZ + NZ + NY) * sizeof(float2);
   // prefetch buffer for the next coil's s_c tile (cp.async) when it does not cost occupancy:
   // keep 2 CTAs/SM where they fit, else (already 1 CTA/SM) stay under the 227 KB limit
-  static constexpr size_t sbytes = (size_t)NYL * NZ * sizeof(float2);
+  // (double-buffered: s_c stays in shared memory for the conj multiply after the inverse)
+  static constexpr size_t sbytes = 2 * (size_t)NYL * NZ * sizeof(float2);
   static constexpr bool PREF = (smem0 + sbytes <= 110 * 1024) || (smem0 > 113 * 1024 && smem0 + sbytes <= 220 * 1024);
   static constexpr size_t smem = smem0 + (PREF ? sbytes : 0);
 };
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
   float2* pt = wb + P::WBS;                          // NYL x NZ: p (or x) tile, natural
   float2* twz = pt + NYL * NZ;                       // NZ
   float2* twy = twz + NZ;                            // NY
-  float2* sbuf = twy + NY;                           // P::PREF: next coil's s_c tile (NYL x NZ)
+  float2* sbuf = twy + NY;                           // P::PREF: [2][NYL x NZ] s_c tiles
   __shared__ double red[32];
   __shared__ int lastflag;
 
@@ -225,11 +226,12 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
         if (mk[(size_t)(g * KB + kbl + NYL * ka) * NZ + tid]) mbits |= 1u << (kbl * G + ka);
   }
   constexpr bool PF = P::PREF && (MATVEC || MODE == KP_ENCODE);
-  auto prefetch_s = [&](int cc) {  // s_cc tile (this CTA's rows) -> sbuf, 16-byte cp.async
+  auto prefetch_s = [&](int cc) {  // s_cc tile (this CTA's rows) -> sbuf[cc & 1], 16-byte cp.async
     const size_t so = ((size_t)b * a.C + cc) * img + (size_t)xpl * PN;
+    float2* dst = sbuf + (cc & 1) * NYL * NZ;
     for (int e = tid; e < NYL * NZ / 2; e += T) {
       const int row = e / (NZ / 2), c2 = e % (NZ / 2);
-      cp_async16(sbuf + row * NZ + 2 * c2, a.sens + so + (size_t)(G * row + g) * NZ + 2 * c2);
+      cp_async16(dst + row * NZ + 2 * c2, a.sens + so + (size_t)(G * row + g) * NZ + 2 * c2);
     }
     cp_async_commit();
   };
@@ -252,7 +254,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
             cp_async_wait_all();
             __syncthreads();
           }
-          v[n1] = cmul(sbuf[r * NZ + z], pt[r * NZ + z]);
+          v[n1] = cmul(sbuf[(c & 1) * NYL * NZ + r * NZ + z], pt[r * NZ + z]);
         } else {
           v[n1] = cmul(a.sens[soff + (size_t)(G * r + g) * NZ + z], pt[r * NZ + z]);
         }
@@ -278,6 +280,13 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
       }
     } else {
       // adjoint: the rows about to be overwritten by peers must be free (previous coil done)
+    }
+    // s_c for the conj multiply after the inverse: from the prefetch buffer, or loaded now so
+    // the L2 latency hides behind the cluster exchange
+    float2 sv[MATVEC && !PF ? N1 : 1];
+    if constexpr (MATVEC && !PF) {
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) sv[n1] = a.sens[soff + (size_t)(G * r + g) * NZ + N2 * n1 + j];
     }
     cl_sync<G>();
     // (3) cross-cluster DFT, pointwise operator, inverse cross-cluster DFT
@@ -366,9 +375,11 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
       }
     } else {
 #pragma unroll
-      for (int n1 = 0; n1 < N1; ++n1) {  // s_c re-read (L2) rather than held across the transform
-        const float2 sv = a.sens[soff + (size_t)(G * r + g) * NZ + N2 * n1 + j];
-        const float2 t = cmulc(sv, v[n1]);
+      for (int n1 = 0; n1 < N1; ++n1) {
+        float2 s1;
+        if constexpr (PF) s1 = sbuf[(c & 1) * NYL * NZ + r * NZ + N2 * n1 + j];
+        else s1 = sv[n1];
+        const float2 t = cmulc(s1, v[n1]);
         acc[n1].x += t.x;
         acc[n1].y += t.y;
       }
