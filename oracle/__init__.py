@@ -14,6 +14,8 @@ Contents (each function cites the PAPER.md passage it follows):
   pcg.py     preconditioned CG
   sb.py      Algorithm 1, literal per-coil k-space data feedback
   dense.py   dense brute-force matrices built from the definitions (pins only)
+  preprocess.py  sensitivity / coil-image normalisation with support masking and SVD coil
+             compression
 
 Everything is float64 / complex128.  Parity pins: see tests/test_oracle_*.py and the
 DESIGN.md "Oracle pins" table.  Nothing here is "parity unpinned" except the end-to-end
