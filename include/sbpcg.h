@@ -200,6 +200,27 @@ void sb_comm_destroy(sb_comm* comm);
 /* Attach (comm != NULL) or detach the communicator; rebuilds Lambda (collective). */
 sb_status sb_pcg_set_comm(sb_ctx* ctx, sb_comm* comm);
 
+/* ------------------------------------------------------------------------------------
+ * Data preprocessing of the paper's Methods (no context; DEVICE pointers only, SB_E_ARG
+ * otherwise; enqueued on `stream`).  Arrays are [batch][coils][npix] complex, npix = the
+ * pixels of one image (any dimensionality).
+ * ------------------------------------------------------------------------------------ */
+/* S_hat_i = [sum_j S_j^H S_j]^{-1/2} S_i, set to 0 outside the subject.
+ * support: uint8 [batch or 1][npix] (support_shared = 1: one for all), NULL = everywhere.
+ * Asynchronous. */
+sb_status sb_normalize_sens(const sb_c64* sens, const uint8_t* support, int32_t batch, int32_t coils, int64_t npix,
+                            int32_t support_shared, sb_c64* sens_out, void* stream);
+/* m_i <- S_hat_i sum_j S_hat_j^H m_j.  Asynchronous; m_out may equal m. */
+sb_status sb_normalize_coil_images(const sb_c64* m, const sb_c64* sens_hat, int32_t batch, int32_t coils, int64_t npix,
+                                   sb_c64* m_out, void* stream);
+/* SVD coil compression (Huang et al. 2008): per problem, the coil
+ * covariance G = sum_n y(n) y(n)^H (fp64), its eigenvectors U (descending eigenvalues), and
+ * A = U[:, :coils_out]^H applied to the data y and the maps: y_out = A y, sens_out = A sens
+ * ([batch][coils_out][npix]).  coils <= 64.  eig_out: optional HOST float [batch][coils].
+ * Synchronous (the C x C eigen-decomposition runs on the host).  Outputs must not alias. */
+sb_status sb_coil_compress(const sb_c64* y, const sb_c64* sens, int32_t batch, int32_t coils, int64_t npix,
+                           int32_t coils_out, sb_c64* y_out, sb_c64* sens_out, float* eig_out, void* stream);
+
 /* Number of kernels launched by this context since creation (for bench.py). */
 int64_t sb_kernel_launch_count(const sb_ctx* ctx);
 

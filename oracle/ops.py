@@ -10,7 +10,8 @@ import numpy as np
 from .fft import fftn_u, ifftn_u
 
 __all__ = ["encode", "encode_adj", "data_normal", "diff", "diff_adj", "tv_normal",
-           "haar_fwd", "haar_inv", "apply_A", "shrink", "rss_init"]
+           "haar_fwd", "haar_inv", "d4_fwd", "d4_inv", "wavelet_fwd", "wavelet_inv", "D4_H",
+           "apply_A", "shrink", "rss_init"]
 
 
 def encode(x, sens, mask):
@@ -106,6 +107,79 @@ def haar_inv(c, levels, nd=None):
             blk = _haar_axis_inv(blk, lead + d)
         out[sl] = blk
     return out
+
+
+# Daubechies 4-tap scaling filter ("Daubechies 4"; reading A32: the 4-coefficient
+# orthonormal wavelet D4), h = [1+r3, 3+r3, 3-r3, 1-r3] / (4 sqrt2); wavelet g_m = (-1)^m h_{3-m}.
+_R3 = np.sqrt(3.0)
+D4_H = np.array([1 + _R3, 3 + _R3, 3 - _R3, 1 - _R3]) / (4 * np.sqrt(2.0))
+D4_G = np.array([D4_H[3], -D4_H[2], D4_H[1], -D4_H[0]])
+
+
+def _d4_axis_fwd(block, ax):
+    """One periodized D4 analysis step along axis `ax`: a_k = sum_m h_m x_{(2k+m) mod n},
+    d_k = sum_m g_m x_{(2k+m) mod n}; approximation first (Mallat)."""
+    n = block.shape[ax]
+    k = np.arange(n // 2)
+    a = sum(D4_H[m] * np.take(block, (2 * k + m) % n, axis=ax) for m in range(4))
+    d = sum(D4_G[m] * np.take(block, (2 * k + m) % n, axis=ax) for m in range(4))
+    return np.concatenate((a, d), axis=ax)
+
+
+def _d4_axis_inv(block, ax):
+    """Synthesis = transpose of the analysis (orthonormal): x_j = sum_k h_{(j-2k) mod n} a_k +
+    g_{(j-2k) mod n} d_k, accumulated tap by tap."""
+    n = block.shape[ax]
+    h = n // 2
+    a = np.take(block, np.arange(h), axis=ax)
+    d = np.take(block, np.arange(h, n), axis=ax)
+    out = np.zeros_like(block)
+    k = np.arange(h)
+    for m in range(4):  # scatter-add tap m (indices repeat when n < 4)
+        np.add.at(np.moveaxis(out, ax, 0), (2 * k + m) % n, np.moveaxis(D4_H[m] * a + D4_G[m] * d, ax, 0))
+    return out
+
+
+def d4_fwd(x, levels, nd=None):
+    """L-level periodized D4 DWT in the Mallat layout of haar_fwd (per level along d0, d1[, d2]
+    on the current approximation block).  Orthonormal: the unitary W of PAPER.md:117."""
+    nd = x.ndim if nd is None else nd
+    shape = x.shape[-nd:]
+    for s_ in shape:
+        if s_ % (1 << levels):
+            raise ValueError("image size not divisible by 2^levels")
+    out = np.array(x, dtype=np.complex128, copy=True)
+    lead = out.ndim - nd
+    for lvl in range(levels):
+        sl = tuple([slice(None)] * lead + [slice(0, s_ >> lvl) for s_ in shape])
+        blk = out[sl]
+        for d in range(nd):
+            blk = _d4_axis_fwd(blk, lead + d)
+        out[sl] = blk
+    return out
+
+
+def d4_inv(c, levels, nd=None):
+    """W^H = W^{-1} for the D4 DWT (coarsest level first, axes in reverse order)."""
+    nd = c.ndim if nd is None else nd
+    shape = c.shape[-nd:]
+    out = np.array(c, dtype=np.complex128, copy=True)
+    lead = out.ndim - nd
+    for lvl in reversed(range(levels)):
+        sl = tuple([slice(None)] * lead + [slice(0, s_ >> lvl) for s_ in shape])
+        blk = out[sl]
+        for d in reversed(range(nd)):
+            blk = _d4_axis_inv(blk, lead + d)
+        out[sl] = blk
+    return out
+
+
+def wavelet_fwd(x, levels, nd=None, family="haar"):
+    return d4_fwd(x, levels, nd) if family == "d4" else haar_fwd(x, levels, nd)
+
+
+def wavelet_inv(c, levels, nd=None, family="haar"):
+    return d4_inv(c, levels, nd) if family == "d4" else haar_inv(c, levels, nd)
 
 
 def apply_A(x, sens, mask, mu, lam, gamma):

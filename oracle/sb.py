@@ -1,7 +1,8 @@
 """Oracle Split Bregman, Algorithm 1 of PAPER.md:136-157, literally (test infrastructure
 only; see oracle/__init__.py).
 
-Readings: A8 literal thresholds 1/lambda and 1/gamma; A9 complex soft
+W is the orthonormal Haar (reading A6) or, with wavelet="d4", the paper's Daubechies-4
+(reading A32).  Readings: A8 literal thresholds 1/lambda and 1/gamma; A9 complex soft
 threshold; A10 anisotropic TV (separate d_x, d_y[, d_z]); A11 all wavelet coefficients
 shrunk; A12 RSS init; A13 nInner = 1 unless given; A14 auxiliaries persist across outer
 iterations; lambda = 0 or gamma = 0 skips that branch.
@@ -35,7 +36,7 @@ class SbLog:
 
 def sb_recon(y, sens, mask, mu, lam, gamma, n_outer, n_inner=1, levels=1, eps=1e-3,
              max_iters=50, precond="circulant", feedback="literal", x_init=None,
-             return_state=False):
+             return_state=False, wavelet="haar"):
     """Algorithm 1.  y: [C, *image] zero-filled k-space, sens: [C, *image],
     mask: 0/1 over the k-space grid.  Returns (x, SbLog[, state])."""
     nd = mask.ndim
@@ -73,7 +74,7 @@ def sb_recon(y, sens, mask, mu, lam, gamma, n_outer, n_inner=1, levels=1, eps=1e
             if lam != 0:
                 rhs = rhs + lam * sum(ops.diff_adj(d[a] - bd[a], a, nd) for a in range(nd))
             if gamma != 0:
-                rhs = rhs + gamma * ops.haar_inv(dw - bw, levels, nd)
+                rhs = rhs + gamma * ops.wavelet_inv(dw - bw, levels, nd, wavelet)
             res = pcg(A, rhs, x, Minv, eps, max_iters)                   # step 5
             x = res.x
             log.pcg_iters.append(res.iters)
@@ -85,7 +86,7 @@ def sb_recon(y, sens, mask, mu, lam, gamma, n_outer, n_inner=1, levels=1, eps=1e
                     d[a] = ops.shrink(z, 1.0 / lam)
                     bd[a] = z - d[a]
             if gamma != 0:                                              # steps 8, 11
-                z = ops.haar_fwd(x, levels, nd) + bw
+                z = ops.wavelet_fwd(x, levels, nd, wavelet) + bw
                 dw = ops.shrink(z, 1.0 / gamma)
                 bw = z - dw
         if feedback == "literal":                                       # steps 13-15

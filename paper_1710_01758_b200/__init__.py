@@ -5,7 +5,8 @@ The binding is loaded on first attribute access so that ``paper_1710_01758_b200.
 be imported (and run) before the library exists; any use of the compute path without the
 built library raises ImportError (there is no CPU fallback)."""
 
-_EXPORTS = ("SbPcg", "SbError", "SbComm", "coil_shard", "abi_version", "LIB_PATH")
+_EXPORTS = ("SbPcg", "SbError", "SbComm", "coil_shard", "normalize_sens", "normalize_coil_images",
+            "coil_compress", "abi_version", "LIB_PATH")
 
 
 def __getattr__(name):

@@ -233,6 +233,20 @@ cudaError_t launch_kp3(int mode, const KPArgs& a, cudaStream_t st);  // 3D plane
 bool kp2_supported(int NY, int NZ);
 bool kp3_supported(int NY, int NZ);
 
+// preprocessing (k_prep.cu)
+cudaError_t launch_normalize_sens(const float2* s, const uint8_t* sup, size_t sup_bstride, int B, int C, size_t npix,
+                                  float2* out, cudaStream_t st);
+cudaError_t launch_normalize_images(const float2* m, const float2* sh, int B, int C, size_t npix, float2* out,
+                                    cudaStream_t st);
+cudaError_t launch_gram(const float2* d, int B, int C, size_t npix, double2* part, int nblk, double2* G,
+                        cudaStream_t st);
+cudaError_t launch_coil_apply(const float2* in, const float2* A, int B, int C, int K, size_t npix, float2* out,
+                              cudaStream_t st);
+}  // namespace sbk
+#include <complex>
+namespace sbk {
+void hermitian_eig(int n, const std::complex<double>* G, double* w, std::complex<double>* U);
+
 cudaError_t launch_lambda_build(const LamArgs& a, cudaStream_t st);
 cudaError_t launch_lambda_chunk(const LamArgs& a, cudaStream_t st);  // L_COL_SENS + L_ROW_ACC only
 cudaError_t launch_lambda_tail(const LamArgs& a, cudaStream_t st);   // from g to k (or kc2)

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -1166,6 +1167,82 @@ sb_status sb_pcg_set_comm(sb_ctx* c, sb_comm* cm) {
   c->comm = cm;
   for (auto& g : c->gs) g.maxit = -1;  // cached graphs do not apply
   return build_lambda(c);               // Lambda from the marginal over all ranks' coils
+}
+
+// ------------------------------------------------------------------ preprocessing (no context)
+sb_status sb_normalize_sens(const sb_c64* sens, const uint8_t* support, int32_t batch, int32_t coils, int64_t npix,
+                            int32_t support_shared, sb_c64* sens_out, void* stream) {
+  if (!sens || !sens_out || batch < 1 || coils < 1 || npix < 1) return SB_E_ARG;
+  if (!is_device_ptr(sens) || !is_device_ptr(sens_out) || (support && !is_device_ptr(support))) return SB_E_ARG;
+  cudaError_t e = launch_normalize_sens((const float2*)sens, support, support_shared ? 0 : (size_t)npix, batch, coils,
+                                        (size_t)npix, (float2*)sens_out, (cudaStream_t)stream);
+  return e == cudaSuccess ? SB_OK : SB_E_CUDA;
+}
+
+sb_status sb_normalize_coil_images(const sb_c64* m, const sb_c64* sens_hat, int32_t batch, int32_t coils, int64_t npix,
+                                   sb_c64* m_out, void* stream) {
+  if (!m || !sens_hat || !m_out || batch < 1 || coils < 1 || npix < 1) return SB_E_ARG;
+  if (!is_device_ptr(m) || !is_device_ptr(sens_hat) || !is_device_ptr(m_out)) return SB_E_ARG;
+  cudaError_t e = launch_normalize_images((const float2*)m, (const float2*)sens_hat, batch, coils, (size_t)npix,
+                                          (float2*)m_out, (cudaStream_t)stream);
+  return e == cudaSuccess ? SB_OK : SB_E_CUDA;
+}
+
+sb_status sb_coil_compress(const sb_c64* y, const sb_c64* sens, int32_t batch, int32_t coils, int64_t npix,
+                           int32_t coils_out, sb_c64* y_out, sb_c64* sens_out, float* eig_out, void* stream) {
+  if (!y || !sens || !y_out || !sens_out || batch < 1 || coils < 1 || coils > 64 || npix < 1 || coils_out < 1 ||
+      coils_out > coils)
+    return SB_E_ARG;
+  if (!is_device_ptr(y) || !is_device_ptr(sens) || !is_device_ptr(y_out) || !is_device_ptr(sens_out)) return SB_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int E = coils * coils;
+  const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(256, npix / 256));
+  double2 *part = nullptr, *G = nullptr;
+  float2* A = nullptr;
+  auto cleanup = [&]() {
+    if (part) cudaFree(part);
+    if (G) cudaFree(G);
+    if (A) cudaFree(A);
+  };
+  if (cudaMalloc(&part, sizeof(double2) * (size_t)batch * nblk * E) != cudaSuccess ||
+      cudaMalloc(&G, sizeof(double2) * (size_t)batch * E) != cudaSuccess ||
+      cudaMalloc(&A, sizeof(float2) * (size_t)batch * coils_out * coils) != cudaSuccess) {
+    cleanup();
+    return SB_E_NOMEM;
+  }
+  // coil covariance of the data (k-space: equal to the image-domain one, F unitary)
+  if (launch_gram((const float2*)y, batch, coils, (size_t)npix, part, nblk, G, st) != cudaSuccess) {
+    cleanup();
+    return SB_E_CUDA;
+  }
+  std::vector<std::complex<double>> hG((size_t)batch * E), U((size_t)E);
+  std::vector<double> w(coils);
+  std::vector<float2> hA((size_t)batch * coils_out * coils);
+  if (cudaMemcpyAsync(hG.data(), G, sizeof(double2) * hG.size(), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    cleanup();
+    return SB_E_CUDA;
+  }
+  for (int b = 0; b < batch; ++b) {
+    hermitian_eig(coils, hG.data() + (size_t)b * E, w.data(), U.data());
+    if (eig_out)
+      for (int k = 0; k < coils; ++k) eig_out[(size_t)b * coils + k] = (float)w[k];
+    for (int k = 0; k < coils_out; ++k)  // A = U[:, :K]^H
+      for (int c = 0; c < coils; ++c) {
+        const std::complex<double> u = std::conj(U[(size_t)c * coils + k]);
+        hA[((size_t)b * coils_out + k) * coils + c] = make_float2((float)u.real(), (float)u.imag());
+      }
+  }
+  if (cudaMemcpyAsync(A, hA.data(), sizeof(float2) * hA.size(), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      launch_coil_apply((const float2*)y, A, batch, coils, coils_out, (size_t)npix, (float2*)y_out, st) != cudaSuccess ||
+      launch_coil_apply((const float2*)sens, A, batch, coils, coils_out, (size_t)npix, (float2*)sens_out, st) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    cleanup();
+    return SB_E_CUDA;
+  }
+  cleanup();
+  return SB_OK;
 }
 
 sb_status sb_pcg_build_precond(sb_ctx* c) {

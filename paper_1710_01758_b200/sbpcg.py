@@ -67,6 +67,10 @@ _sig = {
     "sb_comm_init": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(_vp)]),
     "sb_comm_destroy": (None, [_vp]),
     "sb_pcg_set_comm": (C.c_int, [_vp, _vp]),
+    "sb_normalize_sens": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_int64, C.c_int32, _vp, _vp]),
+    "sb_normalize_coil_images": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_int64, _vp, _vp]),
+    "sb_coil_compress": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_int64, C.c_int32, _vp, _vp,
+                                   C.POINTER(C.c_float), _vp]),
     "sb_pcg_destroy": (None, [_vp]),
     "sb_status_str": (C.c_char_p, [C.c_int]),
     "sb_last_error": (C.c_char_p, [_vp]),
@@ -277,6 +281,57 @@ class SbComm:
             self.close()
         except Exception:
             pass
+
+
+def _stream():
+    return _vp(torch.cuda.current_stream().cuda_stream)
+
+
+def _bcn(t: torch.Tensor):
+    """[B, C, *image] complex64 CUDA tensor -> (B, C, npix)."""
+    if t.dtype != torch.complex64 or not t.is_cuda or t.dim() < 3:
+        raise TypeError("expected a complex64 CUDA tensor [B, C, *image]")
+    return t.shape[0], t.shape[1], int(np.prod(t.shape[2:]))
+
+
+def normalize_sens(sens: torch.Tensor, support: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """S_hat_i = [sum_j S_j^H S_j]^{-1/2} S_i, zero outside `support`."""
+    B, Cc, npx = _bcn(sens)
+    out = torch.empty_like(sens)
+    shared = 0
+    sp = None
+    if support is not None:
+        support = support.contiguous()
+        shared = 1 if support.numel() == npx else 0
+        sp = _ptr(support)
+    st = _lib.sb_normalize_sens(_ptr(sens.contiguous()), sp, B, Cc, npx, shared, _ptr(out), _stream())
+    if st != 0:
+        raise SbError(st, "sb_normalize_sens")
+    return out
+
+
+def normalize_coil_images(m: torch.Tensor, sens_hat: torch.Tensor) -> torch.Tensor:
+    """m_i <- S_hat_i sum_j S_hat_j^H m_j."""
+    B, Cc, npx = _bcn(m)
+    out = torch.empty_like(m)
+    st = _lib.sb_normalize_coil_images(_ptr(m.contiguous()), _ptr(sens_hat.contiguous()), B, Cc, npx, _ptr(out),
+                                       _stream())
+    if st != 0:
+        raise SbError(st, "sb_normalize_coil_images")
+    return out
+
+
+def coil_compress(y: torch.Tensor, sens: torch.Tensor, coils_out: int):
+    """SVD coil compression: returns (y_out, sens_out, eigenvalues [B, C])."""
+    B, Cc, npx = _bcn(y)
+    yo = torch.empty((B, coils_out) + tuple(y.shape[2:]), dtype=torch.complex64, device=y.device)
+    so = torch.empty((B, coils_out) + tuple(sens.shape[2:]), dtype=torch.complex64, device=y.device)
+    ev = (C.c_float * (B * Cc))()
+    st = _lib.sb_coil_compress(_ptr(y.contiguous()), _ptr(sens.contiguous()), B, Cc, npx, int(coils_out), _ptr(yo),
+                               _ptr(so), ev, _stream())
+    if st != 0:
+        raise SbError(st, "sb_coil_compress")
+    return yo, so, torch.tensor(list(ev), dtype=torch.float32).view(B, Cc)
 
 
 def coil_shard(coils: int, rank: int, world: int):

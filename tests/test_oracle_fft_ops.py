@@ -220,3 +220,46 @@ def test_synth_masks_counts():
     m4 = random_vd_mask2d((256, 128), 6, 24, rng_for(4, 0, 2))
     assert m4.sum() == (256 * 128) // 6
     assert np.all(m4[np.ix_((np.arange(24) - 12) % 256, (np.arange(24) - 12) % 128)] == 1)
+
+
+# ------------------------------------------------------- Daubechies-4 W (reading A32)
+@pytest.mark.parametrize("shape,levels", [((8, 8), 1), ((16, 8), 2), ((8, 16), 3), ((8, 4, 8), 2)])
+def test_d4_is_orthonormal_dense(shape, levels):
+    nd = len(shape)
+    Wd = dense.dense_from_op(lambda v: ops.d4_fwd(v, levels, nd), shape)
+    assert np.allclose(Wd.conj().T @ Wd, np.eye(Wd.shape[0]), atol=1e-12)
+    x = np.random.default_rng(2).standard_normal(shape) + 1j * np.random.default_rng(3).standard_normal(shape)
+    assert np.allclose(ops.d4_inv(ops.d4_fwd(x, levels, nd), levels, nd), x, atol=1e-12)
+
+
+def test_d4_filter_identities_and_worked_examples():
+    h, g = ops.D4_H, np.array([ops.D4_H[3], -ops.D4_H[2], ops.D4_H[1], -ops.D4_H[0]])
+    assert np.isclose(h.sum(), np.sqrt(2)) and np.isclose(np.sum(h ** 2), 1.0)   # normalisation
+    assert np.isclose(g.sum(), 0) and np.isclose(np.sum(np.arange(4) * g), 0)    # 2 vanishing moments
+    assert np.isclose(h[0] * h[2] + h[1] * h[3], 0)                               # shift orthogonality
+    # impulse at 0, n = 4 (1D via a 4x1 image along d0): a = (h0, h2), d = (g0, g2)
+    x = np.zeros((4, 1), complex)
+    x[0, 0] = 1
+    c = ops._d4_axis_fwd(x, 0)[:, 0]
+    assert np.allclose(c, [h[0], h[2], g[0], g[2]])
+    # n = 2 reduces to the orthonormal Haar (the filter wraps twice)
+    y = np.array([[3.0 + 1j], [1.0 - 2j]])
+    assert np.allclose(ops._d4_axis_fwd(y, 0), ops._haar_axis_fwd(y, 0))
+    # constants have zero detail coefficients at every level
+    w = ops.d4_fwd(np.full((16, 16), 2.5 + 0.5j), 3)
+    mask = np.zeros((16, 16), bool)
+    mask[:2, :2] = True
+    assert np.max(np.abs(w[~mask])) < 1e-12
+
+
+def test_sb_with_d4_reduces_to_least_squares_when_thresholds_are_huge():
+    # with both weights tiny the thresholds 1/lambda, 1/gamma are huge, every shrink returns 0,
+    # and W enters the iteration only through W^H W = I (b_w = W x, W^H b_w = x): Haar and D4
+    # must give the same SB iterates
+    import synth
+    from oracle import problems, sb
+    p = synth.problem2d(1, 0, shape=(16, 16), coils=2)
+    y = problems.make_kspace(p["phantom"], p["sens"], p["mask"], p["noise"])
+    xa, _ = sb.sb_recon(y, p["sens"], p["mask"], 1.0, 1e-6, 1e-6, 3, 1, 2, 0.0, 40, "circulant", wavelet="haar")
+    xb, _ = sb.sb_recon(y, p["sens"], p["mask"], 1.0, 1e-6, 1e-6, 3, 1, 2, 0.0, 40, "circulant", wavelet="d4")
+    assert np.allclose(xa, xb, atol=1e-10 * np.abs(xa).max())

@@ -16,6 +16,8 @@ for spec in "2 k1_matvec 20" "3 k1_matvec 6" "4 kp_plane 6" "5 kp_plane 3"; do
     -o gpurun_out/prof/full_c$1 -f python tools/prof_step.py --config $1 --eager --steps 1 --warmup 1 > gpurun_out/prof/ncuf$1.log 2>&1
   ncu -i gpurun_out/prof/full_c$1.ncu-rep --page raw --csv > gpurun_out/prof/full_c$1_raw.csv 2>/dev/null
   ncu -i gpurun_out/prof/full_c$1.ncu-rep --page details --csv > gpurun_out/prof/full_c$1_details.csv 2>/dev/null
+  ncu -i gpurun_out/prof/full_c$1.ncu-rep --page source --csv --print-source sass > gpurun_out/prof/full_c${1}_src.csv 2>/dev/null
+  rm -f gpurun_out/prof/full_c$1.ncu-rep
   tail -1 gpurun_out/prof/ncuf$1.log
 done
 ls gpurun_out/prof | head -40
