@@ -95,6 +95,11 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
                         const sb_c64* sens, float mu, float lambda, float gamma,
                         void* cuda_stream);
 
+/* Wavelet family of W in the SB shrink step: 0 = orthonormal Haar (default; reading A6),
+ * 1 = periodized Daubechies-4, the paper's W (reading A32), same Mallat layout
+ * and levels (>= 1).  W^H W = I either way, so A and Lambda do not change. */
+sb_status sb_set_wavelet(sb_ctx* ctx, int32_t family);
+
 /* Rebuild Lambda^{-1} from the context's sens/mask/weights (the preconditioner build of
  * PAPER.md:238 / Table 2, timed by bench.py as part of a step). */
 sb_status sb_pcg_build_precond(sb_ctx* ctx);

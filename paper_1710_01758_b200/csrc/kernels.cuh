@@ -253,6 +253,9 @@ cudaError_t launch_lambda_tail(const LamArgs& a, cudaStream_t st);   // from g t
 cudaError_t launch_lambda_expand3(const Lam3Args& a, cudaStream_t st);
 cudaError_t launch_sb_update(const SbArgs& a, cudaStream_t st);
 cudaError_t launch_sb_update3(const SbArgs& a, cudaStream_t st);
+// Daubechies-4 wavelet part of the SB step (k_wav.cu): rhs += gamma W^H(d_w - b_w), b_w update
+cudaError_t launch_d4_sb(const float2* x, float2* wbuf, float2* bw, float2* rhs, int B, int E0, int E1, int E2, int nd,
+                         int levels, float gamma, cudaStream_t st, int* nlaunch);
 cudaError_t launch_log(const Loop& L, cudaStream_t st);
 
 }  // namespace sbk

@@ -99,6 +99,8 @@ struct sb_ctx {
   sb_comm* comm = nullptr;      // coil-sharded mode (this context holds a coil shard)
   float2* accbuf = nullptr;     // [B][img] partial / all-reduced coil sum
   float* jinv = nullptr;        // Jacobi: 1/diag(A) [B][img] (built on first use)
+  int wavelet = 0;              // 0 Haar (reading A6), 1 Daubechies-4 (reading A32)
+  float2* wbuf = nullptr;       // D4 coefficients [B][img]
   std::vector<float> samp_frac; // sampled fraction f of each problem's mask
   void* lscr[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // Lambda build scratch (kept)
   size_t lscr_bytes[5] = {0, 0, 0, 0, 0};
@@ -505,12 +507,13 @@ static sb_status seq_post(sb_ctx* c, Loop L, cudaStream_t st) {
 static sb_status seq_shrink(sb_ctx* c, int par, cudaStream_t st) {
   SbArgs a;
   memset(&a, 0, sizeof(a));
+  const bool d4 = c->wavelet == 1;
   a.B = c->B;
   a.M = c->M;
   a.N = c->N;
   a.levels = c->L;
   a.lam = c->lam;
-  a.gam = c->gam;
+  a.gam = d4 ? 0.f : c->gam;  // D4: the TV kernel writes the TV part only; k_wav.cu adds gamma W^H(.)
   a.x = c->x;
   a.bx_in = c->bx[par];
   a.by_in = c->by[par];
@@ -526,9 +529,16 @@ static sb_status seq_shrink(sb_ctx* c, int par, cudaStream_t st) {
     a.bz_out = c->bz[1 - par];
     CK(launch_sb_update3(a, st));
     c->launches++;
-    return SB_OK;
+  } else {
+    CK(launch_sb_update(a, st));
   }
-  CK(launch_sb_update(a, st));
+  if (d4 && c->gam != 0.f) {
+    int nl = 0;
+    CK(launch_d4_sb(c->x, c->wbuf, c->bw, c->rhs, c->B, c->D0, c->ndim == 3 ? c->D1 : c->N, c->ndim == 3 ? c->D2 : 1,
+                    c->ndim, c->L, c->gam, st, &nl));
+    c->launches += nl;
+  }
+  if (c->ndim == 3 || d4) return SB_OK;
   c->launches++;
   return SB_OK;
 }
@@ -915,7 +925,8 @@ void sb_pcg_destroy(sb_ctx* c) {
                   c->x, c->r, c->z, c->q, c->p0, c->p1, c->tmp, c->bvec, c->u, c->u1, c->rhs,
                   c->bx[0], c->bx[1], c->by[0], c->by[1], c->bw, c->tmpc, c->stage_in, c->stage_out,
                   c->scal, c->ctl, c->counters, c->P.p0, c->P.p1, c->P.cnt, c->hist, c->log_iters, c->log_relres,
-                  c->pmask, c->tw_y, c->tw_z, c->twd_y, c->twd_z, c->bz[0], c->bz[1], c->accbuf, c->jinv};
+                  c->pmask, c->tw_y, c->tw_z, c->twd_y, c->twd_z, c->bz[0], c->bz[1], c->accbuf, c->jinv,
+                  c->wbuf};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (void* p : c->lscr)
@@ -1242,6 +1253,17 @@ sb_status sb_coil_compress(const sb_c64* y, const sb_c64* sens, int32_t batch, i
     return SB_E_CUDA;
   }
   cleanup();
+  return SB_OK;
+}
+
+sb_status sb_set_wavelet(sb_ctx* c, int32_t family) {
+  sb_status s = check_ready(c);
+  if (s) return s;
+  if (family != 0 && family != 1) return fail(c, SB_E_ARG, "wavelet family must be 0 (Haar) or 1 (D4)");
+  if (family == 1 && c->L < 1) return fail(c, SB_E_DIM, "D4 needs wavelet_levels >= 1");
+  if (family == 1 && !c->wbuf) CK(dalloc(&c->wbuf, (size_t)c->B * c->img));
+  c->wavelet = family;
+  for (auto& g : c->gs) g.maxit = -1;  // the captured shrink step changes
   return SB_OK;
 }
 

@@ -50,6 +50,7 @@ _sig = {
     "sb_pcg_create": (C.c_int, [C.POINTER(_vp), C.POINTER(SbDims), C.c_int32, _vp, _vp, C.c_float,
                                 C.c_float, C.c_float, _vp]),
     "sb_pcg_build_precond": (C.c_int, [_vp]),
+    "sb_set_wavelet": (C.c_int, [_vp, C.c_int32]),
     "sb_pcg_apply_A": (C.c_int, [_vp, _vp, _vp]),
     "sb_pcg_apply_Pinv": (C.c_int, [_vp, _vp, _vp]),
     "sb_encode": (C.c_int, [_vp, _vp, _vp, C.c_int32]),
@@ -105,9 +106,10 @@ class SbPcg:
     circulant preconditioner M^{-1} = F^H diag{k}^{-1} F."""
 
     def __init__(self, sens: torch.Tensor, mask: torch.Tensor, mu: float, lam: float, gamma: float,
-                 levels: int = 1, stream: Optional[torch.cuda.Stream] = None):
+                 levels: int = 1, stream: Optional[torch.cuda.Stream] = None, wavelet: str = "haar"):
         """sens: complex64 [B,C,M,N] (2D) or [B,C,D0,D1,D2] (3D; a 4D tensor is read as 2D);
-        mask: uint8 [B,*image] or [*image] (shared).  3D masks must be constant along D0."""
+        mask: uint8 [B,*image] or [*image] (shared).  3D masks must be constant along D0.
+        wavelet: "haar" (reading A6) or "d4" (the paper's Daubechies-4)."""
         if sens.dtype != torch.complex64 or mask.dtype != torch.uint8:
             raise TypeError("sens must be complex64 [B,C,*image], mask uint8 [B,*image] or [*image]")
         if sens.dim() == 3:
@@ -134,6 +136,11 @@ class SbPcg:
             raise SbError(st, "sb_pcg_create failed")
         self._h = h
         self.mu, self.lam, self.gamma, self.levels = mu, lam, gamma, levels
+        if wavelet not in ("haar", "d4"):
+            raise ValueError("wavelet must be 'haar' or 'd4'")
+        if wavelet == "d4":
+            self._check(_lib.sb_set_wavelet(self._h, 1), "set_wavelet")
+        self.wavelet = wavelet
 
     # ------------------------------------------------------------------
     def _check(self, st: int, what: str):

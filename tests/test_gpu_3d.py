@@ -229,3 +229,15 @@ def test_config4_full_size_sampled():
         assert relerr(ya[b], ops.apply_A(_c32(x[b]), s32, q["mask"], mu, lam, gam)) <= 1e-5
         assert relerr(kg[b], precond.build_k(s32, q["mask"], mu, lam, gam)) <= 1e-6
     ctx.close()
+
+
+def test_3d_sb_recon_d4_fixed_counts():
+    shape, coils, L = (16, 32, 32), 2, 2
+    p = _prob3(shape, coils, amp=300.0)[0]
+    mu, lam, gam = 1.0, 0.01, 0.01
+    ctx = SbPcg(_t(p["sens"][None]), torch.from_numpy(p["mask"][None]).to(DEV), mu, lam, gam, L, wavelet="d4")
+    xg, log = ctx.recon(_t(p["y"][None]), 3, eps=0.0, max_iters=6)
+    ref, _ = sb.sb_recon(_c32(p["y"]), _c32(p["sens"]), p["mask"], mu, lam, gam, 3, 1, L, 0.0, 6, "circulant",
+                         wavelet="d4")
+    assert relerr(_np(xg)[0], ref) <= 1e-3, relerr(_np(xg)[0], ref)
+    ctx.close()

@@ -266,3 +266,25 @@ def test_host_pointer_entry_points_match_device():
                        out=torch.empty((1, 64, 64), dtype=torch.complex64))
     assert torch.equal(x1.cpu(), x2)
     ctx.close()
+
+
+@pytest.mark.parametrize("amp", [100.0, 1000.0])
+def test_sb_recon_d4_fixed_counts(amp):
+    # the paper's wavelet (Daubechies-4; reading A32), shrinkage active
+    ps = batch(1, 2, (64, 64), 4, amp=amp)
+    mu, lam, gam = 1.0, 0.05, 0.05
+    sens = np.stack([p["sens"] for p in ps])
+    masks = np.stack([p["mask"] for p in ps])
+    ctx = SbPcg(_t(sens), torch.from_numpy(masks).to(DEV), mu, lam, gam, 2, wavelet="d4")
+    y = np.stack([p["y"] for p in ps])
+    xg, log = ctx.recon(_t(y), 4, eps=0.0, max_iters=10)
+    xg = _np(xg)
+    for b, p in enumerate(ps):
+        s32 = p["sens"].astype(np.complex64).astype(np.complex128)
+        ref, _ = sb.sb_recon(p["y"].astype(np.complex64).astype(np.complex128), s32, p["mask"], mu, lam, gam,
+                             4, 1, 2, 0.0, 10, "circulant", wavelet="d4")
+        haar, _ = sb.sb_recon(p["y"].astype(np.complex64).astype(np.complex128), s32, p["mask"], mu, lam, gam,
+                              4, 1, 2, 0.0, 10, "circulant", wavelet="haar")
+        assert relerr(xg[b], ref) <= 1e-3, relerr(xg[b], ref)
+        assert relerr(ref, haar) > 10 * relerr(xg[b], ref)  # the test discriminates D4 from Haar
+    ctx.close()

@@ -27,7 +27,7 @@ for cfg in (2, 3, 4, 5):
             return (v[h.index(k)], u[h.index(k)]) if k in h else ("-", "")
         name = g("Kernel Name")[0]
         dur = float(g("gpu__time_duration.sum")[0].replace(",", ""))
-        dur_us = dur / 1e3 if g("gpu__time_duration.sum")[1] == "ns" else dur
+        dur_us = dur * {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(g("gpu__time_duration.sum")[1], 1.0)
         mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         rd = float(g("dram__bytes_read.sum")[0].replace(",", "")) * mult.get(g("dram__bytes_read.sum")[1], 1)
         wr = float(g("dram__bytes_write.sum")[0].replace(",", "")) * mult.get(g("dram__bytes_write.sum")[1], 1)
