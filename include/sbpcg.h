@@ -100,6 +100,11 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
  * and levels (>= 1).  W^H W = I either way, so A and Lambda do not change. */
 sb_status sb_set_wavelet(sb_ctx* ctx, int32_t family);
 
+/* Replace the coil sensitivities (same shape; host or device pointer, copied) and rebuild
+ * Lambda.  The mask, weights, buffers and captured CUDA graphs stay valid,
+ * so a new acquisition with the same geometry reuses the context.  Synchronises the stream. */
+sb_status sb_pcg_update_sens(sb_ctx* ctx, const sb_c64* sens);
+
 /* Rebuild Lambda^{-1} from the context's sens/mask/weights (the preconditioner build of
  * PAPER.md:238 / Table 2, timed by bench.py as part of a step). */
 sb_status sb_pcg_build_precond(sb_ctx* ctx);

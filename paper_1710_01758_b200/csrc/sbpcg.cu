@@ -1060,7 +1060,12 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
     }
     // the fused one-kernel preconditioner (KP_PRE2D) is slower than the three column/row
     // passes at the BASELINE sizes (measured: config 3 83k vs 135k it/s), so it is opt-in
-    c->pre2d = kp2_supported((int)M, (int)N) && env_flag("SBPCG_PRE2D", false);
+    // ... except for small batches, where one cluster kernel per problem beats three
+    // launches (config 2: 19.1k vs 17.8k it/s); SBPCG_PRE2D=0/1 forces either
+    const int gpre = M <= 32 ? 1 : (M <= 64 ? 2 : (M <= 128 ? 4 : (M == 256 ? 16 : 8)));
+    const bool small = (int64_t)c->B * gpre <= 2 * 148;
+    const char* pe = getenv("SBPCG_PRE2D");
+    c->pre2d = kp2_supported((int)M, (int)N) && (pe ? pe[0] == '1' : small);
     if (sep && cudaMemcpy(c->rowmask, rm.data(), rm.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(SB_E_CUDA);
   } else {
@@ -1265,6 +1270,20 @@ sb_status sb_set_wavelet(sb_ctx* c, int32_t family) {
   c->wavelet = family;
   for (auto& g : c->gs) g.maxit = -1;  // the captured shrink step changes
   return SB_OK;
+}
+
+sb_status sb_pcg_update_sens(sb_ctx* c, const sb_c64* sens) {
+  sb_status s = check_ready(c);
+  if (s) return s;
+  if (!sens) return fail(c, SB_E_ARG, "update_sens: null");
+  const size_t bytes = (size_t)c->B * c->C * c->img * sizeof(float2);
+  CK(cudaMemcpyAsync(c->sens, sens, bytes, is_device_ptr(sens) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     c->st));
+  if (c->jinv) {  // Jacobi diagonal depends on the maps: rebuilt on next use
+    cudaFree(c->jinv);
+    c->jinv = nullptr;
+  }
+  return build_lambda(c);
 }
 
 sb_status sb_pcg_build_precond(sb_ctx* c) {

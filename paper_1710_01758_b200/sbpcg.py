@@ -51,6 +51,7 @@ _sig = {
                                 C.c_float, C.c_float, _vp]),
     "sb_pcg_build_precond": (C.c_int, [_vp]),
     "sb_set_wavelet": (C.c_int, [_vp, C.c_int32]),
+    "sb_pcg_update_sens": (C.c_int, [_vp, _vp]),
     "sb_pcg_apply_A": (C.c_int, [_vp, _vp, _vp]),
     "sb_pcg_apply_Pinv": (C.c_int, [_vp, _vp, _vp]),
     "sb_encode": (C.c_int, [_vp, _vp, _vp, C.c_int32]),
@@ -165,6 +166,15 @@ class SbPcg:
                            pin_memory=(dev.type == "cpu" and torch.cuda.is_available()))
 
     # ------------------------------------------------------------------ operators
+    def update_sens(self, sens: torch.Tensor):
+        """New coil maps (same shape; host or device) for this context; rebuilds Lambda."""
+        if sens.dim() == self.ndim + 1:
+            sens = sens.unsqueeze(0)
+        if tuple(sens.shape) != tuple(self._sens.shape) or sens.dtype != torch.complex64:
+            raise ValueError("update_sens: shape/dtype must match the context")
+        sens = sens.contiguous()
+        self._check(_lib.sb_pcg_update_sens(self._h, _ptr(sens)), "update_sens")
+
     def build_precond(self):
         self._check(_lib.sb_pcg_build_precond(self._h), "build_precond")
 

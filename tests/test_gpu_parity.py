@@ -288,3 +288,28 @@ def test_sb_recon_d4_fixed_counts(amp):
         assert relerr(xg[b], ref) <= 1e-3, relerr(xg[b], ref)
         assert relerr(ref, haar) > 10 * relerr(xg[b], ref)  # the test discriminates D4 from Haar
     ctx.close()
+
+
+def test_update_sens_equals_fresh_context():
+    # a context reused for new coil maps (same geometry/mask): Lambda rebuilt, cached graphs
+    # still valid; results equal a context created from the new maps
+    ps = batch(2, 2, (128, 128), 6)
+    mask = ps[0]["mask"]
+    ctx = SbPcg(_t(ps[0]["sens"][None]), torch.from_numpy(mask[None]).to(DEV), 1.0, 0.02, 0.02, 3)
+    y1 = make_problem(2, (128, 128), 6, slice_=1)
+    yk = _t(problems_kspace(ps[1], mask)[None])
+    ctx.recon(yk, 2, eps=1e-4, max_iters=30)           # captures graphs with the old maps
+    ctx.update_sens(_t(ps[1]["sens"][None]))
+    xa, la = ctx.recon(yk, 3, eps=1e-4, max_iters=30)
+    fresh = SbPcg(_t(ps[1]["sens"][None]), torch.from_numpy(mask[None]).to(DEV), 1.0, 0.02, 0.02, 3)
+    xb, lb = fresh.recon(yk, 3, eps=1e-4, max_iters=30)
+    assert la["pcg_iters"] == lb["pcg_iters"]
+    assert torch.equal(xa, xb)
+    assert np.array_equal(ctx.get_k().numpy(), fresh.get_k().numpy())
+    del y1
+    ctx.close(), fresh.close()
+
+
+def problems_kspace(p, mask):
+    from oracle import problems
+    return problems.make_kspace(p["phantom"], p["sens"], mask, p["noise"])
