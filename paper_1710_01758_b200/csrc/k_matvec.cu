@@ -317,6 +317,7 @@ static cudaError_t launch_k1_t(const K1Args& a, const CUtensorMap* tmap, int G, 
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return e;
     attr_done = true;
   }
   return launch_ex(kern, dim3(G, a.N / W, a.B), dim3(Split<M>::N2 * W), smem, st, G, *tmap, a);
@@ -350,7 +351,7 @@ int k1_default_W(int M, int N) { return (N % 8 == 0) ? 8 : 4; }
 
 cudaError_t launch_k1(int mode, const K1Args& a, const CUtensorMap* tmap, int W, int G,
                       cudaStream_t st) {
-  if (a.M % G != 0 || a.N % W != 0 || G > 8) return cudaErrorInvalidValue;
+  if (a.M % G != 0 || a.N % W != 0 || G > 16) return cudaErrorInvalidValue;
   switch (a.M) {
     case 8: return launch_k1_m<8>(mode, a, tmap, W, G, st);
     case 16: return launch_k1_m<16>(mode, a, tmap, W, G, st);
