@@ -47,7 +47,8 @@ typedef struct { float re, im; } sb_c64;
 typedef enum {
   SB_OK = 0,
   SB_E_ARG = 1,              /* NULL/aliased/misaligned pointer, bad option value      */
-  SB_E_DIM = 2,              /* shape/batch/coils/levels inconsistent (levels must     */
+  SB_E_DIM = 2,              /* shape/batch/coils/levels inconsistent, or batch*coils  */
+                             /* > 65535 (launch-grid limit); levels must              */
                              /* divide the shape, PAPER.md:117 W unitary on the grid) */
   SB_E_UNSUPPORTED_SIZE = 3, /* an image axis is not in the FFT size set               */
   SB_E_PARAM = 4,            /* gamma <= 0, mu < 0 or lambda < 0 (k >= gamma > 0)      */

@@ -958,6 +958,8 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
       if (Lv > 3 || d % T || T % (1 << Lv)) return SB_E_DIM;
     }
   }
+  // launch-grid limits: coil passes put B*C images (and K1/K1P put B problems) on grid.y/z
+  if ((int64_t)dims->batch * coils > 65535 || (d3 && D0 > 65535)) return SB_E_DIM;
   if (!(gamma > 0.f) || mu < 0.f || lambda < 0.f || !std::isfinite(mu) || !std::isfinite(lambda) ||
       !std::isfinite(gamma))
     return SB_E_PARAM;
