@@ -129,7 +129,7 @@ typedef struct {
   int32_t max_iters;  /* >= 1                                                              */
   int32_t precond;    /* 0 none, 1 circulant, 2 Jacobi z = r/diag(A) with  */
                       /* diag(A) = mu f sum_c |S_c|^2 + 2 nd lambda + gamma (PAPER.md:187;  */
-                      /* f = sampled fraction; built on first use)                         */
+                      /* f = sampled fraction; built on first use; not in coil-sharded mode)*/
   int32_t use_graph;  /* 1: device-driven loop in a CUDA graph (conditional while node)   */
 } sb_pcg_opts;
 

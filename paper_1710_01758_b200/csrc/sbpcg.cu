@@ -1401,6 +1401,8 @@ sb_status sb_adjoint(sb_ctx* c, const sb_c64* y, sb_c64* x) {
 static sb_status check_opts(sb_ctx* c, const sb_pcg_opts* o) {
   if (!o || o->max_iters < 1 || !(o->eps >= 0.f) || o->precond < 0 || o->precond > 2)
     return fail(c, SB_E_ARG, "bad pcg options");
+  if (o->precond == 2 && c->comm)  // diag(A) needs sum_c |S_c|^2 over every rank's coils
+    return fail(c, SB_E_UNSUPPORTED_SIZE, "Jacobi preconditioner is not available in the coil-sharded mode");
   if (o->precond == 2 && !c->jinv) {  // Jacobi diagonal, once
     CK(dalloc(&c->jinv, (size_t)c->B * c->img));
     float* fr = nullptr;
