@@ -96,8 +96,7 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
 
   if (g == 0 && tile == 0 && tid == 0 && a.L.cnt != nullptr) atomicAdd(&a.L.cnt->k1_problems, 1ull);
 
-  // ---- prologue: the p tile (+halo) into shared memory.  Loads are issued in batches
-  // with no global store in between (the x / p_k stores follow in phase 2), so they overlap.
+  // ---- prologue: the p tile (+halo) into shared memory, in batches of independent loads.
   // PCG forms p_k = z + beta p_{k-1} (standard PCG) and x += alpha p_{k-1}.
   const int rows_per = M / G;
   const int r0 = g * rows_per;
@@ -106,13 +105,17 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
   const float2* pold = pidx ? a.pbuf0 : a.pbuf1;
   float2* pnew = pidx ? a.pbuf1 : a.pbuf0;
   const bool need_old = (MODE == K1_PCG) && !first;
+  // one pass over the tile: p_k into shared memory, and for this CTA's own rows (non-halo
+  // columns) also p_k -> pnew and the deferred x += alpha_{k-1} p_{k-1} (p_{k-1} is read once)
   for (int c0 = 0; c0 < PE; c0 += CH) {
-    float2 zz[CH], po[CH];
+    float2 zz[CH], po[CH], xv[CH];
+    bool own[CH];
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
       const int e = (c0 + i) * NT + tid;
       zz[i] = make_float2(0.f, 0.f);
       po[i] = make_float2(0.f, 0.f);
+      own[i] = false;
       if (c0 + i < PE && e < M * PW) {
         const int row = e / PW, cc = e % PW;
         int gcol = col0 + cc - 1;
@@ -121,6 +124,8 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
         if constexpr (MODE == K1_PCG) {
           zz[i] = a.z[gi];
           if (need_old) po[i] = pold[gi];
+          own[i] = cc >= 1 && cc <= W && row >= r0 && row < r0 + rows_per;
+          if (own[i] && need_old) xv[i] = a.x[gi];
         } else {
           zz[i] = a.vin[gi];
         }
@@ -129,41 +134,22 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
       const int e = (c0 + i) * NT + tid;
-      if (c0 + i < PE && e < M * PW)
-        pt[e] = need_old ? make_float2(zz[i].x + (float)beta * po[i].x, zz[i].y + (float)beta * po[i].y) : zz[i];
-    }
-  }
-  __syncthreads();
-  if constexpr (MODE == K1_PCG) {
-    // phase 2: this CTA's rows x W columns: p_k -> pnew, x += alpha_{k-1} p_{k-1}
-    constexpr int OE = (M * W + NT - 1) / NT;  // upper bound of own elements per thread
-    const int own = rows_per * W;
-    constexpr int CH2 = OE < 8 ? OE : 8;
-    for (int c0 = 0; c0 < OE; c0 += CH2) {
-      float2 xv[CH2], po[CH2];
-#pragma unroll
-      for (int i = 0; i < CH2; ++i) {
-        const int e = (c0 + i) * NT + tid;
-        if (need_old && c0 + i < OE && e < own) {
-          const size_t gi = boff + (size_t)(r0 + e / W) * N + col0 + e % W;
-          xv[i] = a.x[gi];
-          po[i] = pold[gi];
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < CH2; ++i) {
-        const int e = (c0 + i) * NT + tid;
-        if (c0 + i < OE && e < own) {
-          const int row = r0 + e / W, cc = e % W;
-          const size_t gi = boff + (size_t)row * N + col0 + cc;
-          pnew[gi] = pt[row * PW + cc + 1];
-          if (need_old) {
-            a.x[gi] = make_float2(xv[i].x + (float)alpha_prev * po[i].x, xv[i].y + (float)alpha_prev * po[i].y);
+      if (c0 + i < PE && e < M * PW) {
+        const float2 p = need_old ? make_float2(zz[i].x + (float)beta * po[i].x, zz[i].y + (float)beta * po[i].y)
+                                  : zz[i];
+        pt[e] = p;
+        if constexpr (MODE == K1_PCG) {
+          if (own[i]) {
+            const size_t gi = boff + (size_t)(e / PW) * N + col0 + (e % PW) - 1;
+            pnew[gi] = p;
+            if (need_old)
+              a.x[gi] = make_float2(xv[i].x + (float)alpha_prev * po[i].x, xv[i].y + (float)alpha_prev * po[i].y);
           }
         }
       }
     }
   }
+  __syncthreads();
 
   // ---- coil loop
   float2 acc[N1];
