@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
   float* rm = reinterpret_cast<float*>(tw + M);                      // [M]
   uint64_t* bar = reinterpret_cast<uint64_t*>(rm + M + (M & 1));     // [2]
   __shared__ double red[32];
+  __shared__ double cred[32];  // cluster pre-reduction slots (rank 0), 2 per CTA
   __shared__ int lastflag;
 
   const int G = gridDim.x;
@@ -267,14 +268,34 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
       }
     }
   }
-  if (G > 1) cluster.sync();  // peers finished reading this CTA's accb
-
-  if constexpr (MODE == K1_APPLY) return;
-  const double s0 = block_sum(d0, red);
+  if constexpr (MODE == K1_APPLY) {
+    if (G > 1) cluster.sync();  // peers finished reading this CTA's accb
+    return;
+  }
+  // block sums, then a fixed-order pre-reduction over the cluster through DSMEM: one partial
+  // (and one arrival atomic) per cluster instead of one per CTA
+  double s0 = block_sum(d0, red);
   double s1 = 0.0;
   if constexpr (MODE == K1_RESID) s1 = block_sum(d1, red);
-  const int nblk = gridDim.x * gridDim.y;
-  const bool last = publish_and_check_last(s0, s1, a.P, b, tile * G + g, nblk, &lastflag);
+  if (G > 1) {
+    if (tid == 0) {
+      double* r0 = cluster.map_shared_rank(cred, 0);
+      r0[2 * g] = s0;
+      r0[2 * g + 1] = s1;
+    }
+    cluster.sync();  // also: peers finished reading this CTA's accb
+    if (g != 0) return;
+    if (tid == 0) {
+      s0 = 0.0;
+      s1 = 0.0;
+      for (int gg = 0; gg < G; ++gg) {
+        s0 += cred[2 * gg];
+        s1 += cred[2 * gg + 1];
+      }
+    }
+  }
+  const int nblk = gridDim.y;  // one publisher per cluster (tile)
+  const bool last = publish_and_check_last(s0, s1, a.P, b, tile, nblk, &lastflag);
   if (!last) return;
   if (tid < 32) {
     const double t0 = warp_sum_partials(a.P.p0 + (size_t)b * a.P.cap, nblk);

@@ -422,6 +422,20 @@ __global__ void k_log(const Loop L) {
   if (threadIdx.x == 0) L.ctl->solve_idx = slot + 1;
 }
 
+// Spin for ~ns nanoseconds (globaltimer): launched before the start event of a timed kernel so
+// the event is timestamped after the kernel was submitted (bench.py roofline timing only).
+__global__ void k_spin(unsigned long long ns) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  unsigned long long t = t0;
+  while (t - t0 < ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+}
+
+cudaError_t launch_spin(cudaStream_t st, unsigned long long ns) {
+  k_spin<<<1, 32, 0, st>>>(ns);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_log(const Loop& L, cudaStream_t st) {
   const int nt = L.B >= 1024 ? 1024 : ((L.B + 31) / 32) * 32;
   return launch_ex(k_log, dim3(1), dim3(nt), 0, st, 0, L);

@@ -257,5 +257,6 @@ cudaError_t launch_sb_update3(const SbArgs& a, cudaStream_t st);
 cudaError_t launch_d4_sb(const float2* x, float2* wbuf, float2* bw, float2* rhs, int B, int E0, int E1, int E2, int nd,
                          int levels, float gamma, cudaStream_t st, int* nlaunch);
 cudaError_t launch_log(const Loop& L, cudaStream_t st);
+cudaError_t launch_spin(cudaStream_t st, unsigned long long ns);
 
 }  // namespace sbk

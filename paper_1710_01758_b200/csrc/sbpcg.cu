@@ -308,6 +308,7 @@ static cudaEvent_t ev_get(sb_ctx* c) {
 static sb_status run_k1(sb_ctx* c, int mode, const K1Args& a, cudaStream_t st) {
   int e0 = -1;
   if (c->timing) {
+    CK(launch_spin(st, 20000));  // start event after the kernel is queued (no submission latency)
     e0 = (int)c->evnext;
     CK(cudaEventRecord(ev_get(c), st));
   }
@@ -325,6 +326,7 @@ static sb_status run_kp(sb_ctx* c, int mode, const KPArgs& a, cudaStream_t st) {
   const bool timed = c->timing && (mode == KP_APPLY || mode == KP_PCG || mode == KP_RESID);
   int e0 = -1;
   if (timed) {
+    CK(launch_spin(st, 20000));  // start event after the kernel is queued (no submission latency)
     e0 = (int)c->evnext;
     CK(cudaEventRecord(ev_get(c), st));
   }
