@@ -44,6 +44,46 @@ template <int S, typename V> __device__ __forceinline__ V mul_si(V a) {
   else return {a.y, -a.x};
 }
 
+// fp32 complex arithmetic on the packed f32x2 pipe (sm_100: FADD2 / FMUL2 / FFMA2 process the
+// (re, im) pair in one instruction; swaps and half negations fold into operand modifiers).
+// Scalar FP32 instructions issue at half the FP32 lane rate on this architecture, and the FFT
+// kernels are FP32-issue bound, so every hot complex operation goes through these overloads
+// (the templates above remain for double2).  Rounding per lane is that of the scalar ops.
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  const float2 t = __fmul2_rn(make_float2(a.x, a.x), b);
+  return __ffma2_rn(make_float2(-a.y, a.y), make_float2(b.y, b.x), t);
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // conj(a) * b
+  const float2 t = __fmul2_rn(make_float2(a.x, a.x), b);
+  return __ffma2_rn(make_float2(a.y, -a.y), make_float2(b.y, b.x), t);
+}
+__device__ __forceinline__ float2 cmul_conjb(float2 a, float2 b) {  // a * conj(b)
+  const float2 t = __fmul2_rn(make_float2(b.x, b.x), a);
+  return __ffma2_rn(make_float2(b.y, -b.y), make_float2(a.y, a.x), t);
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
+// a + conj-free complex multiply-add: acc + a * b
+__device__ __forceinline__ float2 cfma(float2 a, float2 b, float2 acc) {
+  const float2 t = __ffma2_rn(make_float2(a.x, a.x), b, acc);
+  return __ffma2_rn(make_float2(-a.y, a.y), make_float2(b.y, b.x), t);
+}
+// acc + conj(a) * b
+__device__ __forceinline__ float2 cfmac(float2 a, float2 b, float2 acc) {
+  const float2 t = __ffma2_rn(make_float2(a.x, a.x), b, acc);
+  return __ffma2_rn(make_float2(a.y, -a.y), make_float2(b.y, b.x), t);
+}
+#else
+__host__ __device__ inline float2 cfma(float2 a, float2 b, float2 acc) {
+  return {acc.x + a.x * b.x - a.y * b.y, acc.y + a.x * b.y + a.y * b.x};
+}
+__host__ __device__ inline float2 cfmac(float2 a, float2 b, float2 acc) {
+  return {acc.x + a.x * b.x + a.y * b.y, acc.y + a.x * b.y - a.y * b.x};
+}
+#endif
+
 // ------------------------------------------------------------------ compile-time trig
 // cos/sin of 2*pi*e/n evaluated in constexpr double (octant reduction + Taylor series),
 // so register-DFT twiddles become instruction immediates.
@@ -100,11 +140,23 @@ __device__ __forceinline__ V twc(V v) {
     constexpr T h = T(0.70710678118654752440);
     constexpr T c = T(kcos2pi(e, N) > 0 ? 1 : -1);
     constexpr T s = T((ksin2pi(e, N) > 0 ? 1 : -1) * S);
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
+    if constexpr (std::is_same<T, float>::value) {  // (c h + i s h)(v): packed constant multiply
+      const float2 t = __fmul2_rn(make_float2(c * h, c * h), v);
+      return __ffma2_rn(make_float2(-s * h, s * h), make_float2(v.y, v.x), t);
+    }
+#endif
     // (a+ib)(c + i s) * h
     return {h * (c * v.x - s * v.y), h * (s * v.x + c * v.y)};
   } else {
     constexpr T c = T(kcos2pi(e, N));
     constexpr T s = T(S * ksin2pi(e, N));
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
+    if constexpr (std::is_same<T, float>::value) {
+      const float2 t = __fmul2_rn(make_float2(c, c), v);
+      return __ffma2_rn(make_float2(-s, s), make_float2(v.y, v.x), t);
+    }
+#endif
     return {v.x * c - v.y * s, v.x * s + v.y * c};
   }
 }
@@ -137,8 +189,8 @@ template <int S> struct Dft<3, S> {
     constexpr T h = T(0.86602540378443864676);  // sqrt(3)/2
     V a = x[0], b = x[1], c = x[2];
     V s = cadd(b, c), d = csub(b, c);
-    V m = {a.x - T(0.5) * s.x, a.y - T(0.5) * s.y};
-    V t = mul_si<S>(V{h * d.x, h * d.y});
+    V m = csub(a, cscale(s, T(0.5)));
+    V t = mul_si<S>(cscale(d, h));
     x[0] = cadd(a, s);
     x[1] = cadd(m, t);
     x[2] = csub(m, t);

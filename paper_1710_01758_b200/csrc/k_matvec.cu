@@ -182,15 +182,11 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
 #pragma unroll
     for (int q = 0; q < N1; ++q) {
       const float r = rm[specidx<M>(j, q)];
-      v[q] = make_float2(v[q].x * r, v[q].y * r);
+      v[q] = cscale(v[q], r);
     }
     fft_inv<M, Lay>(v, xch, tw, j, l);
 #pragma unroll
-    for (int n1 = 0; n1 < N1; ++n1) {
-      const float2 t = cmulc(s[n1], v[n1]);
-      acc[n1].x += t.x;
-      acc[n1].y += t.y;
-    }
+    for (int n1 = 0; n1 < N1; ++n1) acc[n1] = cfmac(s[n1], v[n1], acc[n1]);  // acc += conj(s_c) v
   }
 
   // ---- coil-group reduction (DSMEM) + epilogue

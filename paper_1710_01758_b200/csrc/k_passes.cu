@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(RowCfg<N, LINES_>::NT) k_row(const PassArgs a)
     }
     fft_fwd<N, typename R::Lay>(v, xch, tw, j, line);
 #pragma unroll
-    for (int s = 0; s < N1; ++s) v[s] = make_float2(v[s].x * lv[s], v[s].y * lv[s]);
+    for (int s = 0; s < N1; ++s) v[s] = cscale(v[s], lv[s]);
     fft_inv<N, typename R::Lay>(v, xch, tw, j, line);
     if (in_range) {
 #pragma unroll

@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
             } else {
               f = ((mbits >> (kbl * G + ka)) & 1u) ? a.scale : 0.f;
             }
-            w[ka] = make_float2(w[ka].x * f, w[ka].y * f);
+            w[ka] = cscale(w[ka], f);
           }
         }
         if constexpr (MODE == KP_ENCODE) {
@@ -368,9 +368,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) {
         const float2 sv = a.sens[soff + (size_t)(G * r + g) * NZ + N2 * n1 + j];
-        const float2 t = cmulc(sv, v[n1]);
-        acc[n1].x += t.x;
-        acc[n1].y += t.y;
+        acc[n1] = cfmac(sv, v[n1], acc[n1]);
         rss[n1] += v[n1].x * v[n1].x + v[n1].y * v[n1].y;
       }
     } else {
@@ -379,9 +377,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
         float2 s1;
         if constexpr (PF) s1 = sbuf[(c & 1) * NYL * NZ + r * NZ + N2 * n1 + j];
         else s1 = sv[n1];
-        const float2 t = cmulc(s1, v[n1]);
-        acc[n1].x += t.x;
-        acc[n1].y += t.y;
+        acc[n1] = cfmac(s1, v[n1], acc[n1]);  // acc += conj(s_c) v
       }
     }
     __syncthreads();  // exchange reads done before the next coil writes wb
