@@ -325,6 +325,50 @@ __device__ __forceinline__ void fft_inv(V (&v)[Split<N>::N1], V* xch, const V* _
   Dft<N1, +1>::run(v);
 }
 
+// Register-twiddle variants for square splits (N1 == N2): thread j's forward twiddles
+// W_N^{j k1} (k1 < N1) and inverse twiddles conj(W_N^{n2 j}) (n2 < N2) are the same N1 values,
+// loaded once per kernel into twr[m] = W_N^{j m} instead of from shared memory per transform.
+template <int N, typename V>
+__device__ __forceinline__ void load_twr(V (&twr)[Split<N>::N1], const V* __restrict__ tw, int j) {
+  static_assert(Split<N>::N1 == Split<N>::N2, "square split only");
+#pragma unroll
+  for (int m = 0; m < Split<N>::N1; ++m) twr[m] = tw[j * m];
+}
+template <int N, typename Lay, typename V>
+__device__ __forceinline__ void fft_fwd_r(V (&v)[Split<N>::N1], V* xch, const V (&twr)[Split<N>::N1], int j,
+                                          int line) {
+  constexpr int N1 = Split<N>::N1, N2 = Split<N>::N2;
+  static_assert(N1 == N2, "square split only");
+  Dft<N1, -1>::run(v);
+#pragma unroll
+  for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], twr[k1]);
+#pragma unroll
+  for (int k1 = 0; k1 < N1; ++k1) xch[Lay::off(k1, j, line)] = v[k1];
+  __syncthreads();
+  V u[N2];
+#pragma unroll
+  for (int n2 = 0; n2 < N2; ++n2) u[n2] = xch[Lay::off(j, n2, line)];
+  Dft<N2, -1>::run(u);
+#pragma unroll
+  for (int k2 = 0; k2 < N2; ++k2) v[k2] = u[k2];
+}
+template <int N, typename Lay, typename V>
+__device__ __forceinline__ void fft_inv_r(V (&v)[Split<N>::N1], V* xch, const V (&twr)[Split<N>::N1], int j,
+                                          int line) {
+  constexpr int N1 = Split<N>::N1, N2 = Split<N>::N2;
+  static_assert(N1 == N2, "square split only");
+  V u[N2];
+#pragma unroll
+  for (int k2 = 0; k2 < N2; ++k2) u[k2] = v[k2];
+  Dft<N2, +1>::run(u);
+#pragma unroll
+  for (int n2 = 0; n2 < N2; ++n2) xch[Lay::off(j, n2, line)] = (n2 == 0 || j == 0) ? u[n2] : cmul_conjb(u[n2], twr[n2]);
+  __syncthreads();
+#pragma unroll
+  for (int k1 = 0; k1 < N1; ++k1) v[k1] = xch[Lay::off(k1, j, line)];
+  Dft<N1, +1>::run(v);
+}
+
 // spectral index held in slot s of thread j (layout B)
 template <int N> __device__ __forceinline__ int specidx(int j, int s) {
   constexpr int N1 = Split<N>::N1, N2 = Split<N>::N2;

@@ -153,6 +153,9 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
   __syncthreads();
 
   // ---- coil loop
+  constexpr bool TWR = (N1 == N2);  // square split: twiddles in registers (fft_core.cuh)
+  float2 twr[N1];
+  if constexpr (TWR) load_twr<M>(twr, tw, j);
   float2 acc[N1];
 #pragma unroll
   for (int i = 0; i < N1; ++i) acc[i] = make_float2(0.f, 0.f);
@@ -172,7 +175,8 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
       const int row = natidx<M>(j, n1);
       v[n1] = cmul(s[n1], pt[row * PW + l + 1]);
     }
-    fft_fwd<M, Lay>(v, xch, tw, j, l);
+    if constexpr (TWR) fft_fwd_r<M, Lay>(v, xch, twr, j, l);
+    else fft_fwd<M, Lay>(v, xch, tw, j, l);
     // every thread has read ring[stage] before the barrier inside fft_fwd
     if (tid == 0 && ci + 2 < ncoil) {
       const int c = g + (ci + 2) * G;
@@ -184,7 +188,8 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
       const float r = rm[specidx<M>(j, q)];
       v[q] = cscale(v[q], r);
     }
-    fft_inv<M, Lay>(v, xch, tw, j, l);
+    if constexpr (TWR) fft_inv_r<M, Lay>(v, xch, twr, j, l);
+    else fft_inv<M, Lay>(v, xch, tw, j, l);
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) acc[n1] = cfmac(s[n1], v[n1], acc[n1]);  // acc += conj(s_c) v
   }
