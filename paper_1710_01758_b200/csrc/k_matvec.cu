@@ -156,6 +156,9 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
   constexpr bool TWR = (N1 == N2);  // square split: twiddles in registers (fft_core.cuh)
   float2 twr[N1];
   if constexpr (TWR) load_twr<M>(twr, tw, j);
+  float rmr[N1];  // this thread's spectral rows' mask factors r/M, fixed for the kernel
+#pragma unroll
+  for (int q = 0; q < N1; ++q) rmr[q] = rm[specidx<M>(j, q)];
   float2 acc[N1];
 #pragma unroll
   for (int i = 0; i < N1; ++i) acc[i] = make_float2(0.f, 0.f);
@@ -184,10 +187,7 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
       tma_load_3d(ring + stage * TILE, &tmap, 2 * col0, 0, b * a.C + c, &bar[stage]);
     }
 #pragma unroll
-    for (int q = 0; q < N1; ++q) {
-      const float r = rm[specidx<M>(j, q)];
-      v[q] = cscale(v[q], r);
-    }
+    for (int q = 0; q < N1; ++q) v[q] = cscale(v[q], rmr[q]);
     if constexpr (TWR) fft_inv_r<M, Lay>(v, xch, twr, j, l);
     else fft_inv<M, Lay>(v, xch, tw, j, l);
 #pragma unroll
