@@ -91,8 +91,10 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
   constexpr bool MATVEC = (MODE == KP_APPLY || MODE == KP_PCG || MODE == KP_RESID);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* wb = reinterpret_cast<float2*>(smem_raw);  // P::WBS: row exchange / tile spectra
+  // the p (or x) tile exists only in the modes that multiply by it (matvec, encode)
+  constexpr bool HAS_PT = (MODE == KP_APPLY || MODE == KP_PCG || MODE == KP_RESID || MODE == KP_ENCODE);
   float2* pt = wb + P::WBS;                          // NYL x NZ: p (or x) tile, natural
-  float2* twz = pt + NYL * NZ;                       // NZ
+  float2* twz = pt + (HAS_PT ? NYL * NZ : 0);        // NZ
   float2* twy = twz + NZ;                            // NY
   float2* sbuf = twy + NY;                           // P::PREF: [2][NYL x NZ] s_c tiles
   __shared__ double red[32];
@@ -533,15 +535,18 @@ template <int NY, int NZ, int G, int MODE>
 static cudaError_t kp_launch(const KPArgs& a, cudaStream_t st) {
   using P = PlaneCfg<NY, NZ, G>;
   auto kern = kp_plane<NY, NZ, G, MODE>;
+  constexpr bool HAS_PT = (MODE == KP_APPLY || MODE == KP_PCG || MODE == KP_RESID || MODE == KP_ENCODE);
+  constexpr bool PF = P::PREF && (MODE == KP_APPLY || MODE == KP_PCG || MODE == KP_RESID || MODE == KP_ENCODE);
+  constexpr size_t smem = P::smem0 - (HAS_PT ? 0 : (size_t)P::NYL * NZ * sizeof(float2)) + (PF ? P::sbytes : 0);
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (G > 8 && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
       return e;
     attr_done = true;
   }
-  return launch_ex(kern, dim3(G, a.planes, a.B), dim3(P::T), P::smem, st, G > 1 ? G : 0, a);
+  return launch_ex(kern, dim3(G, a.planes, a.B), dim3(P::T), smem, st, G > 1 ? G : 0, a);
 }
 
 // cluster size per plane height: the column DFT holds NY/G <= 32 values and G | NY/G
