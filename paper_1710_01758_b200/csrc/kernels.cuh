@@ -120,6 +120,20 @@ struct SbArgs {
   float2* bz_out;
 };
 
+// Persistent per-problem cluster PCG (k_pcgc.cu): 256 x 256 line-mask problems, circulant M.
+struct KcArgs {
+  int B, C, N;
+  float mu, lam, gam;
+  const float* rmask;      // [B or 1][M] = r/M
+  int rmask_bstride;
+  const float* lam_inv;    // [B][M][N] = 1/(N k)
+  float2 *x, *r, *z, *pbuf0, *pbuf1, *tmp;
+  const float2* tw;        // [M] forward twiddles
+  Loop L;
+};
+bool kc_supported(int M, int N);
+cudaError_t launch_kc(const KcArgs& a, const CUtensorMap* tmap16, cudaStream_t st);
+
 // Plane kernels (k_plane*.cu): one G-CTA cluster per NY x NZ plane, DSMEM-exchanged 2D FFT.
 enum KPMode { KP_APPLY = 0, KP_PCG = 1, KP_RESID = 2, KP_PRECOND = 3, KP_ENCODE = 4, KP_ADJOINT = 5,
               KP_PRE2D = 6 };

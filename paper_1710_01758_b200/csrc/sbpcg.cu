@@ -134,6 +134,8 @@ struct sb_ctx {
   float* log_relres = nullptr;
   int log_cap = 0;
   CUtensorMap tmap;
+  CUtensorMap tmap16;           // 16-column coil-map boxes for the persistent cluster PCG (KC)
+  bool kc = false;              // KC enabled: 256x256 line masks, single GPU (k_pcgc.cu)
   // graphs: 0 = solve, 1 = recon first, 2/3 = recon next (parity)
   GraphSlot gs[4];
   sb_status sticky = SB_OK;
@@ -194,7 +196,9 @@ static std::vector<V> make_tw(int n) {
 }
 
 // ------------------------------------------------------------------ TMA descriptor
-static sb_status make_tmap(sb_ctx* c) {
+static sb_status make_tmap_w(sb_ctx* c, CUtensorMap* out, int W);
+static sb_status make_tmap(sb_ctx* c) { return make_tmap_w(c, &c->tmap, c->W); }
+static sb_status make_tmap_w(sb_ctx* c, CUtensorMap* out, int W) {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
   CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
@@ -202,9 +206,9 @@ static sb_status make_tmap(sb_ctx* c) {
   auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   cuuint64_t gdim[3] = {(cuuint64_t)(2 * c->N), (cuuint64_t)c->M, (cuuint64_t)c->B * c->C};
   cuuint64_t gstride[2] = {(cuuint64_t)c->N * 8, (cuuint64_t)c->M * c->N * 8};
-  cuuint32_t box[3] = {(cuuint32_t)(2 * c->W), (cuuint32_t)c->M, 1};
+  cuuint32_t box[3] = {(cuuint32_t)(2 * W), (cuuint32_t)c->M, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(&c->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)c->sens, gdim, gstride, box, estr,
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)c->sens, gdim, gstride, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(c, SB_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
@@ -332,6 +336,44 @@ static sb_status run_kp(sb_ctx* c, int mode, const KPArgs& a, cudaStream_t st) {
   }
   CK(c->ndim == 3 ? launch_kp3(mode, a, st) : launch_kp2(mode, a, st));
   if (timed) {
+    int e1 = (int)c->evnext;
+    CK(cudaEventRecord(ev_get(c), st));
+    c->evpend.push_back({0, {e0, e1}});
+  }
+  c->launches++;
+  return SB_OK;
+}
+
+// The whole PCG loop of every problem in one persistent launch (one 16-CTA cluster per
+// problem); timed like K1 for the roofline, units = PCG iterations (counted by the kernel).
+static sb_status run_kc(sb_ctx* c, Loop L, cudaStream_t st) {
+  KcArgs a;
+  memset(&a, 0, sizeof(a));
+  a.B = c->B;
+  a.C = c->C;
+  a.N = c->N;
+  a.mu = c->mu;
+  a.lam = c->lam;
+  a.gam = c->gam;
+  a.rmask = c->rowmask;
+  a.rmask_bstride = c->mask_shared ? 0 : c->M;
+  a.lam_inv = c->lam_inv;
+  a.x = c->x;
+  a.r = c->r;
+  a.z = c->z;
+  a.pbuf0 = c->p0;
+  a.pbuf1 = c->p1;
+  a.tmp = c->tmp;
+  a.tw = c->tw_m;
+  a.L = L;
+  int e0 = -1;
+  if (c->timing) {
+    CK(launch_spin(st, 20000));
+    e0 = (int)c->evnext;
+    CK(cudaEventRecord(ev_get(c), st));
+  }
+  CK(launch_kc(a, &c->tmap16, st));
+  if (c->timing) {
     int e1 = (int)c->evnext;
     CK(cudaEventRecord(ev_get(c), st));
     c->evpend.push_back({0, {e0, e1}});
@@ -606,9 +648,10 @@ static sb_status build_graph(sb_ctx* c, int kind, const sb_pcg_opts* o, const fl
   }
   cudaGraph_t G;
   CK(cudaGraphCreate(&G, 0));
-  cudaGraphConditionalHandle h;
-  CK(cudaGraphConditionalHandleCreate(&h, G, 0, 0));
-  Loop L = make_loop(c, (unsigned long long)h);
+  const bool kcp = c->kc && o->precond == 1;  // persistent cluster PCG: no conditional node
+  cudaGraphConditionalHandle h = 0;
+  if (!kcp) CK(cudaGraphConditionalHandleCreate(&h, G, 0, 0));
+  Loop L = make_loop(c, kcp ? 0ull : (unsigned long long)h);
   cudaStream_t cs = c->cap1;
   int64_t l0 = c->launches;
   bool saved_timing = c->timing;
@@ -636,6 +679,26 @@ static sb_status build_graph(sb_ctx* c, int kind, const sb_pcg_opts* o, const fl
     cudaStreamEndCapture(cs, &dummy);
     c->timing = saved_timing;
     return s;
+  }
+  if (kcp) {
+    const int64_t lb = c->launches;
+    s = run_kc(c, L, cs);
+    if (!s) s = seq_post(c, L, cs);
+    cudaGraph_t Gout;
+    cudaError_t e3 = cudaStreamEndCapture(cs, &Gout);
+    c->timing = saved_timing;
+    if (s) return s;
+    CK(e3);
+    CK(cudaGraphInstantiate(&g.exec, G, 0));
+    g.graph = G;
+    g.nbody = 0;
+    g.nfixed = (int)(c->launches - l0);
+    (void)lb;
+    c->launches = l0;
+    g.eps = o->eps;
+    g.maxit = o->max_iters;
+    g.precond = o->precond;
+    return SB_OK;
   }
   cudaStreamCaptureStatus cst;
   const cudaGraphNode_t* deps = nullptr;
@@ -703,6 +766,10 @@ static sb_status eager_solve(sb_ctx* c, int kind, const sb_pcg_opts* o, const fl
   }
   if (s) return s;
   if ((s = seq_precond(c, L, o->precond, 0, c->r, c->z, st))) return s;
+  if (c->kc && o->precond == 1) {  // persistent cluster PCG
+    if ((s = run_kc(c, L, st))) return s;
+    return seq_post(c, L, st);
+  }
   int host_any = 1;
   CK(cudaMemcpyAsync(&host_any, &c->ctl->any_active, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1134,6 +1201,12 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   c->k1_bytes = 8.0 * (double)img * c->C + 48.0 * (double)img +
                 (c->separable ? 4.0 * c->M : (double)(d3 ? (size_t)D1 * D2 : img));
   sb_status s = c->plane ? SB_OK : make_tmap(c);  // K1 streams the coil maps by TMA
+  // the persistent cluster PCG for 256x256 line-mask problems: opt-in (SBPCG_KC=1). Measured
+  // slower than the kernel sequence on B200 (config 2 18.0k vs 19.8k it/s: one 16-CTA cluster
+  // per slice runs the 12 coils serially on 16 SMs; config 3 128k vs 173k: per-slice
+  // iteration imbalance leaves clusters idle at the end of a launch)
+  c->kc = !d3 && c->separable && kc_supported(c->M, c->N) && c->C >= 1 && env_flag("SBPCG_KC", false);
+  if (!s && c->kc) s = make_tmap_w(c, &c->tmap16, 16);
   if (s) {
     sb_pcg_destroy(c);
     return s;
@@ -1615,7 +1688,9 @@ sb_status sb_get_kernel_time(sb_ctx* c, int32_t which, double* ms, int64_t* laun
     // + z, p_{k-1} (and halo), x read + x, p_k, q written (6 x 8N) + row mask (4M);
     // averaged over the timed launches using the device count of active problems.
     const double N = (double)c->img;
-    const double per = which == 0 ? c->k1_bytes : (4.0 * 8.0 * N + 4.0 * N);
+    // KC (persistent PCG): one unit = one PCG iteration, B_iter = 8N(C+10) + 4N + 4M
+    const double per = which == 0 ? (c->kc ? 8.0 * N * (c->C + 10) + 4.0 * N + 4.0 * c->M : c->k1_bytes)
+                                  : (4.0 * 8.0 * N + 4.0 * N);
     Counters h{};
     if (cudaMemcpy(&h, c->counters, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return fail(c, SB_E_CUDA, "counters");
     const double probs = (which == 0 && c->t_n[0] > 0) ? (double)h.k1_problems / (double)c->t_n[0] : (double)c->B;
