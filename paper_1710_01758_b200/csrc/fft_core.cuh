@@ -50,30 +50,34 @@ template <int S, typename V> __device__ __forceinline__ V mul_si(V a) {
 // kernels are FP32-issue bound, so every hot complex operation goes through these overloads
 // (the templates above remain for double2).  Rounding per lane is that of the scalar ops.
 #if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
+// Operand placement matters: the swapped / half-negated vector goes in operand A (folded as
+// .LO_HI.NP) and the real factor in operand B as a scalar broadcast (.F32), so a complex
+// multiply is exactly FMUL2 + FFMA2 with no register moves.
+__device__ __forceinline__ float2 bc(float s) { return make_float2(s, s); }
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  const float2 t = __fmul2_rn(make_float2(a.x, a.x), b);
-  return __ffma2_rn(make_float2(-a.y, a.y), make_float2(b.y, b.x), t);
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {  // a * b
+  const float2 t = __fmul2_rn(b, bc(a.x));
+  return __ffma2_rn(make_float2(-b.y, b.x), bc(a.y), t);
 }
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // conj(a) * b
-  const float2 t = __fmul2_rn(make_float2(a.x, a.x), b);
-  return __ffma2_rn(make_float2(a.y, -a.y), make_float2(b.y, b.x), t);
+  const float2 t = __fmul2_rn(b, bc(a.x));
+  return __ffma2_rn(make_float2(b.y, -b.x), bc(a.y), t);
 }
 __device__ __forceinline__ float2 cmul_conjb(float2 a, float2 b) {  // a * conj(b)
-  const float2 t = __fmul2_rn(make_float2(b.x, b.x), a);
-  return __ffma2_rn(make_float2(b.y, -b.y), make_float2(a.y, a.x), t);
+  const float2 t = __fmul2_rn(a, bc(b.x));
+  return __ffma2_rn(make_float2(a.y, -a.x), bc(b.y), t);
 }
-__device__ __forceinline__ float2 cscale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
-// a + conj-free complex multiply-add: acc + a * b
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return __fmul2_rn(a, bc(s)); }
+// acc + a * b
 __device__ __forceinline__ float2 cfma(float2 a, float2 b, float2 acc) {
-  const float2 t = __ffma2_rn(make_float2(a.x, a.x), b, acc);
-  return __ffma2_rn(make_float2(-a.y, a.y), make_float2(b.y, b.x), t);
+  const float2 t = __ffma2_rn(b, bc(a.x), acc);
+  return __ffma2_rn(make_float2(-b.y, b.x), bc(a.y), t);
 }
 // acc + conj(a) * b
 __device__ __forceinline__ float2 cfmac(float2 a, float2 b, float2 acc) {
-  const float2 t = __ffma2_rn(make_float2(a.x, a.x), b, acc);
-  return __ffma2_rn(make_float2(a.y, -a.y), make_float2(b.y, b.x), t);
+  const float2 t = __ffma2_rn(b, bc(a.x), acc);
+  return __ffma2_rn(make_float2(b.y, -b.x), bc(a.y), t);
 }
 #else
 __host__ __device__ inline float2 cfma(float2 a, float2 b, float2 acc) {
@@ -142,8 +146,8 @@ __device__ __forceinline__ V twc(V v) {
     constexpr T s = T((ksin2pi(e, N) > 0 ? 1 : -1) * S);
 #if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
     if constexpr (std::is_same<T, float>::value) {  // (c h + i s h)(v): packed constant multiply
-      const float2 t = __fmul2_rn(make_float2(c * h, c * h), v);
-      return __ffma2_rn(make_float2(-s * h, s * h), make_float2(v.y, v.x), t);
+      const float2 t = __fmul2_rn(v, bc(c * h));
+      return __ffma2_rn(make_float2(-v.y, v.x), bc(s * h), t);
     }
 #endif
     // (a+ib)(c + i s) * h
@@ -153,8 +157,8 @@ __device__ __forceinline__ V twc(V v) {
     constexpr T s = T(S * ksin2pi(e, N));
 #if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
     if constexpr (std::is_same<T, float>::value) {
-      const float2 t = __fmul2_rn(make_float2(c, c), v);
-      return __ffma2_rn(make_float2(-s, s), make_float2(v.y, v.x), t);
+      const float2 t = __fmul2_rn(v, bc(c));
+      return __ffma2_rn(make_float2(-v.y, v.x), bc(s), t);
     }
 #endif
     return {v.x * c - v.y * s, v.x * s + v.y * c};
