@@ -23,14 +23,16 @@ __device__ __forceinline__ float2 shrinkc(float2 z, float t) {
   return make_float2(z.x * s, z.y * s);
 }
 
+// TT = max tile edge: 32, or 16 when a 32-tile grid would leave SMs idle (one 256^2 slice)
+template <int TT>
 __global__ void __launch_bounds__(256) k_sb_update(const SbArgs a) {
-  __shared__ float2 xs[SBT + 2][SBT + 2];
-  __shared__ float2 vx[SBT + 1][SBT];
-  __shared__ float2 vy[SBT][SBT + 1];
-  __shared__ float2 wa[SBT][SBT];
-  __shared__ float2 wv[SBT][SBT];
+  __shared__ float2 xs[TT + 2][TT + 2];
+  __shared__ float2 vx[TT + 1][TT];
+  __shared__ float2 vy[TT][TT + 1];
+  __shared__ float2 wa[TT][TT];
+  __shared__ float2 wv[TT][TT];
   const int M = a.M, N = a.N, L = a.levels;
-  const int TH = M < SBT ? M : SBT, TW = N < SBT ? N : SBT;
+  const int TH = M < TT ? M : TT, TW = N < TT ? N : TT;
   const int i0 = blockIdx.x * TH, j0 = blockIdx.y * TW, b = blockIdx.z;
   const size_t img = (size_t)M * N, boff = (size_t)b * img;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -198,7 +200,10 @@ __global__ void __launch_bounds__(256) k_sb_update(const SbArgs a) {
 cudaError_t launch_sb_update(const SbArgs& a, cudaStream_t st) {
   const int TH = a.M < SBT ? a.M : SBT, TW = a.N < SBT ? a.N : SBT;
   if (a.M % TH || a.N % TW || (TH % (1 << a.levels)) || (TW % (1 << a.levels))) return cudaErrorInvalidValue;
-  return launch_ex(k_sb_update, dim3(a.M / TH, a.N / TW, a.B), dim3(256), 0, st, 0, a);
+  const bool small = (int64_t)(a.M / TH) * (a.N / TW) * a.B < 2 * 148;
+  if (small && a.M >= 16 && a.N >= 16 && a.M % 16 == 0 && a.N % 16 == 0 && (16 % (1 << a.levels)) == 0)
+    return launch_ex(k_sb_update<16>, dim3(a.M / 16, a.N / 16, a.B), dim3(256), 0, st, 0, a);
+  return launch_ex(k_sb_update<SBT>, dim3(a.M / TH, a.N / TW, a.B), dim3(256), 0, st, 0, a);
 }
 
 }  // namespace sbk
