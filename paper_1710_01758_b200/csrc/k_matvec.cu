@@ -99,8 +99,10 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
 
   // ---- prologue: the p tile (+halo) into shared memory, in batches of independent loads.
   // PCG forms p_k = z + beta p_{k-1} (standard PCG) and x += alpha p_{k-1}.
-  const int rows_per = M / G;
-  const int r0 = g * rows_per;
+  // rows of the epilogue owned by this CTA (G need not divide M: the last CTAs take fewer)
+  const int rows_ceil = (M + G - 1) / G;
+  const int r0 = min(M, g * rows_ceil);
+  const int rows_per = min(rows_ceil, M - r0);
   constexpr int PE = (M * PW + NT - 1) / NT;  // elements per thread
   constexpr int CH = PE < 10 ? PE : 10;
   const float2* pold = pidx ? a.pbuf0 : a.pbuf1;
@@ -280,9 +282,9 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
   if constexpr (MODE == K1_RESID) s1 = block_sum(d1, red);
   if (G > 1) {
     if (tid == 0) {
-      double* r0 = cluster.map_shared_rank(cred, 0);
-      r0[2 * g] = s0;
-      r0[2 * g + 1] = s1;
+      double* rk0 = cluster.map_shared_rank(cred, 0);
+      rk0[2 * g] = s0;
+      rk0[2 * g + 1] = s1;
     }
     cluster.sync();  // also: peers finished reading this CTA's accb
     if (g != 0) return;
@@ -359,7 +361,7 @@ int k1_default_W(int M, int N) { return (N % 8 == 0) ? 8 : 4; }
 
 cudaError_t launch_k1(int mode, const K1Args& a, const CUtensorMap* tmap, int W, int G,
                       cudaStream_t st) {
-  if (a.M % G != 0 || a.N % W != 0 || G > 16) return cudaErrorInvalidValue;
+  if (a.N % W != 0 || G > 16 || G < 1) return cudaErrorInvalidValue;
   switch (a.M) {
     case 8: return launch_k1_m<8>(mode, a, tmap, W, G, st);
     case 16: return launch_k1_m<16>(mode, a, tmap, W, G, st);

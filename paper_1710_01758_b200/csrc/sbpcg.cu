@@ -1193,7 +1193,7 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
     if (g <= c->C && c->M % g == 0 && (int64_t)c->B * tiles * g <= 2 * 148) c->G = g;
   if (const char* ge = getenv("SBPCG_K1_G")) {  // debugging override of the coil-group count
     const int g = atoi(ge);
-    if (g >= 1 && g <= 8 && g <= c->C && c->M % g == 0) c->G = g;
+    if (g >= 1 && g <= 16) c->G = g;  // G need not divide M (uneven rows); g > C leaves idle CTAs
   }
   // algorithmic bytes per problem-launch of the matvec: coil maps
   // 8NC + z, p_{k-1}, x read + p_k, x, q written (6 x 8N) + the mask (4M floats for line
