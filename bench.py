@@ -383,6 +383,40 @@ def run_ours(args):
     value = it_sum / (t_max / 1e3)
     ms_per_step = t_max / args.steps
 
+    # ---- per-PCG-iteration rate and HBM fraction (BASELINE north_star target: ">= 60% of the
+    # B200 HBM roofline per PCG iteration"): fixed-count solves (eps = 0, CUDA graph) with
+    # K = 10 and 50 iterations, t_iter = (t50 - t10) / 40 (SURVEY 8(d) timing procedure; the
+    # prelude/post of a solve cancel), best of 3; bytes per iteration = B_iter of SURVEY 8(a),
+    # 8N(C+10) + 4N + mask bytes, per problem
+    pcg_iter = None
+    if not coil_mode:
+        bsolve = ctx.adjoint(y_d)
+        x0 = torch.zeros_like(bsolve)
+
+        def t_solve(K):
+            best = float("inf")
+            for _ in range(3):
+                flush.fill_(1.0)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                ctx.solve(bsolve, x0, eps=0.0, max_iters=K, precond=args.precond, use_graph=use_graph)
+                e1.record(st)
+                e1.synchronize()
+                best = min(best, e0.elapsed_time(e1))
+            return best
+        t_solve(10)  # graph capture
+        t10, t50 = t_solve(10), t_solve(50)
+        t_it = max(t50 - t10, 1e-9) / 40.0 / 1e3  # s
+        nimg = int(np.prod(spec.shape))
+        mask_b = 4.0 * spec.shape[0] if spec.mask_kind == "lines" else float(np.prod(spec.shape[1:] if len(spec.shape) == 3 else spec.shape))
+        b_iter = per * (8.0 * nimg * (spec.coils + 10) + 4.0 * nimg + mask_b)
+        pk, _ = peaks()
+        pcg_iter = {"us_per_iteration": t_it * 1e6, "problem_iters_per_s": per / t_it,
+                    "bytes_per_iteration": b_iter, "achieved_gbs": b_iter / t_it / 1e9,
+                    "hbm_frac": b_iter / t_it / 1e9 / pk,
+                    "method": "fixed-count solves (eps=0) K=10 and K=50, (t50-t10)/40, best of 3, L2 flushed"}
+
     # ---- dominant-kernel roofline: K1 (fused matvec) timed with CUDA events per launch on the
     # context stream (eager mode for this pass)
     ctx.set_kernel_timing(True)
@@ -473,6 +507,7 @@ def run_ours(args):
                                     else "kp_plane (cluster plane matvec: per-coil 2D FFT via DSMEM)"),
                          "kernel_avg_us": k_avg_s * 1e6, "kernel_launches_timed": k_n,
                          "alg_bytes_per_launch": k_bytes},
+            "pcg_iteration": pcg_iter,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
