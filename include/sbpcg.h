@@ -200,7 +200,7 @@ sb_status sb_get_kernel_time(sb_ctx* ctx, int32_t which /*0 = matvec K1, 1 = pre
  * bitwise identical across ranks, so no scalar all-reduce is needed).  Lambda's coil
  * marginal, u_1 and the RSS init are all-reduced as well.  The PCG loop is host-driven in
  * this mode (no CUDA graph).  NCCL is loaded at run time (the process's libnccl.so.2, or
- * SBPCG_NCCL_LIB).  Requires the plane path (ndim = 3, or a non-separable 2D mask).
+ * SBPCG_NCCL_LIB).  For ndim = 3 contexts (2D batches shard by slice, with no collective).
  * ------------------------------------------------------------------------------------ */
 typedef struct sb_comm sb_comm;
 /* rank 0: a 128-byte NCCL unique id to broadcast to the other ranks (out of band). */

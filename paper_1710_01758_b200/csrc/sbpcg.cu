@@ -1255,7 +1255,9 @@ void sb_comm_destroy(sb_comm* cm) {
 sb_status sb_pcg_set_comm(sb_ctx* c, sb_comm* cm) {
   sb_status s = check_ready(c);
   if (s) return s;
-  if (!c->plane) return fail(c, SB_E_UNSUPPORTED_SIZE, "coil sharding needs the plane path (3D or non-separable 2D)");
+  // coil sharding is the 3D (BASELINE config 5) mode: its Lambda marginal, u_1 / RSS init and
+  // adjoint all-reduce across ranks; the 2D paths are slice-sharded instead (no collective)
+  if (c->ndim != 3) return fail(c, SB_E_UNSUPPORTED_SIZE, "coil sharding is for 3D contexts (slice-shard 2D batches)");
   if (cm && !c->accbuf) CK(dalloc(&c->accbuf, (size_t)c->B * c->img));
   c->comm = cm;
   for (auto& g : c->gs) g.maxit = -1;  // cached graphs do not apply
