@@ -45,3 +45,22 @@ def test_coil_mode_world1_equals_unsharded():
     assert la["pcg_iters"] == lb["pcg_iters"]
     assert relerr(xb.cpu().numpy(), xa.cpu().numpy()) <= 1e-5
     a.close(), b.close(), comm.close()
+
+
+def test_coil_mode_guards():
+    # coil sharding is the 3D mode; Jacobi needs every rank's coils and is rejected there
+    from paper_1710_01758_b200 import SbError
+    comm = SbComm(SbComm.unique_id(), 0, 1)
+    p2 = synth.problem2d(1, 0, shape=(32, 32), coils=2)
+    m2 = synth.random_vd_mask2d((32, 32), 4, 4, synth.rng_for(1, 0, 9))
+    c2 = SbPcg(torch.from_numpy(p2["sens"][None]).to(torch.complex64).cuda(), torch.from_numpy(m2[None]).cuda(),
+               1.0, 0.02, 0.02, 1)
+    with pytest.raises(SbError):
+        c2.set_comm(comm)
+    c2.close()
+    p3 = synth.problem3d(5, shape=(8, 32, 32), coils=2)
+    c3 = _ctx(p3, comm)
+    b = torch.ones((1, 8, 32, 32), dtype=torch.complex64, device="cuda")
+    with pytest.raises(SbError):
+        c3.solve(b, torch.zeros_like(b), eps=1e-4, max_iters=5, precond=2)
+    c3.close(), comm.close()
