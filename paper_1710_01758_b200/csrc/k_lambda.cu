@@ -10,6 +10,8 @@
 // Outputs k (fp64, parity) and Lambda^{-1} = 1/(N k) (fp32; the 1/N of the unnormalised
 // inverse FFT used by the preconditioner kernels is folded in).
 // FLOPs (Table 1): C forward 2D FFTs of the coil maps plus 3 FFTs.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace sbk {
@@ -130,11 +132,16 @@ __global__ void __launch_bounds__(LRow<N>::NT) k_lrow(const LamArgs a) {
   __syncthreads();
   double2 v[N1];
   if constexpr (KIND == L_ROW_ACC) {
-    const int b = blockIdx.y;
+    // coils [c0, c1) of problem b: all of them (csplit = 1), or one of csplit groups whose
+    // partial sums are added in a fixed order by k_lacc_sum
+    const int S = a.csplit > 1 ? a.csplit : 1;
+    const int b = blockIdx.y / S, sg = blockIdx.y % S;
+    const int per = (a.C + S - 1) / S;
+    const int c0 = sg * per, c1 = min(a.C, c0 + per);
     double acc[N1];
 #pragma unroll
     for (int s = 0; s < N1; ++s) acc[s] = 0.0;
-    for (int c = 0; c < a.C; ++c) {
+    for (int c = c0; c < c1; ++c) {
       const double2* t = a.tmp + ((size_t)b * a.C + c) * img + (size_t)row * N;
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) v[n1] = t[natidx<N>(j, n1)];
@@ -145,12 +152,18 @@ __global__ void __launch_bounds__(LRow<N>::NT) k_lrow(const LamArgs a) {
     }
     const double inv = 1.0 / ((double)img * (double)img);
     if (in_range) {
-      double2* g = a.g + (size_t)b * img + (size_t)row * N;
+      if (S > 1) {
+        double* gp = a.gpart + ((size_t)b * S + sg) * img + (size_t)row * N;
 #pragma unroll
-      for (int s = 0; s < N1; ++s) {
-        const int k = specidx<N>(j, s);
-        const double prev = a.accumulate ? g[k].x : 0.0;
-        g[k] = make_double2(prev + acc[s] * inv, 0.0);
+        for (int s = 0; s < N1; ++s) gp[specidx<N>(j, s)] = acc[s] * inv;
+      } else {
+        double2* g = a.g + (size_t)b * img + (size_t)row * N;
+#pragma unroll
+        for (int s = 0; s < N1; ++s) {
+          const int k = specidx<N>(j, s);
+          const double prev = a.accumulate ? g[k].x : 0.0;
+          g[k] = make_double2(prev + acc[s] * inv, 0.0);
+        }
       }
     }
   } else if constexpr (KIND == L_ROW_G || KIND == L_ROW_MASK) {
@@ -182,6 +195,16 @@ __global__ void __launch_bounds__(LRow<N>::NT) k_lrow(const LamArgs a) {
   }
 }
 
+// g[b] (+)= sum over the csplit coil groups in fixed order
+__global__ void __launch_bounds__(256) k_lacc_sum(const LamArgs a, size_t img) {
+  const int b = blockIdx.y, S = a.csplit;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < img; i += (size_t)gridDim.x * blockDim.x) {
+    double t = a.accumulate ? a.g[(size_t)b * img + i].x : 0.0;
+    for (int sg = 0; sg < S; ++sg) t += a.gpart[((size_t)b * S + sg) * img + i];
+    a.g[(size_t)b * img + i] = make_double2(t, 0.0);
+  }
+}
+
 template <int M, int KIND>
 static cudaError_t lcol(const LamArgs& a, int nimg, cudaStream_t st) {
   k_lcol<M, KIND><<<dim3(a.N / LW, nimg), LCol<M>::NT, 0, st>>>(a);
@@ -193,11 +216,29 @@ static cudaError_t lrow(const LamArgs& a, int nimg, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// the coil accumulation pass, split over up to 16 coil groups (gpart holds B x 16 images) when
+// B x rows alone would leave SMs idle
+template <int N>
+static cudaError_t row_acc(const LamArgs& a0, cudaStream_t st) {
+  LamArgs a = a0;
+  const int ctas = (a.M + LRow<N>::LINES - 1) / LRow<N>::LINES * a.B;
+  a.csplit = (a.gpart != nullptr) ? std::max(1, std::min(std::min(a.C, 16), (2 * 148 + ctas - 1) / ctas)) : 1;
+  cudaError_t e;
+  if ((e = lrow<N, L_ROW_ACC>(a, a.B * a.csplit, st))) return e;
+  if (a.csplit > 1) {
+    const size_t img = (size_t)a.M * a.N;
+    k_lacc_sum<<<dim3((unsigned)std::min<size_t>(1024, (img + 255) / 256), a.B), 256, 0, st>>>(a, img);
+    e = cudaGetLastError();
+    if (a.nextra) ++*a.nextra;
+  }
+  return e;
+}
+
 template <int M, int N>
 static cudaError_t chunk_mn(const LamArgs& a, cudaStream_t st) {
   cudaError_t e;
   if ((e = lcol<M, L_COL_SENS>(a, a.B * a.C, st))) return e;
-  return lrow<N, L_ROW_ACC>(a, a.B, st);
+  return row_acc<N>(a, st);
 }
 template <int M, int N>
 static cudaError_t tail_mn(const LamArgs& a, cudaStream_t st) {
@@ -214,7 +255,7 @@ template <int M, int N>
 static cudaError_t build_mn(const LamArgs& a, cudaStream_t st) {
   cudaError_t e;
   if ((e = lcol<M, L_COL_SENS>(a, a.B * a.C, st))) return e;
-  if ((e = lrow<N, L_ROW_ACC>(a, a.B, st))) return e;
+  if ((e = row_acc<N>(a, st))) return e;
   if ((e = lcol<M, L_COL_G>(a, a.B, st))) return e;
   if ((e = lrow<N, L_ROW_G>(a, a.B, st))) return e;
   if ((e = lcol<M, L_COL_MASK>(a, a.nmask, st))) return e;

@@ -88,6 +88,9 @@ struct LamArgs {
   // 3D (readout-constant mask): the planes of every coil are fed
   // as extra "coils" of a 2D build in chunks; g accumulates over chunks.
   int accumulate;          // L_ROW_ACC: g += instead of g =
+  int csplit;              // L_ROW_ACC: coils split over csplit CTA groups (partials in gpart)
+  double* gpart;           // [B][csplit][M][N] partial coil sums (fixed-order reduction)
+  int* nextra;             // host counter: +1 per extra (partial-sum) launch, may be null
   int d3;                  // final pass writes k_c (2D, fp64) to kc2 instead of k / Lambda^{-1}
   double* kc2;             // [B][D1*D2]
 };

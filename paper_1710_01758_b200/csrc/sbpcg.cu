@@ -102,8 +102,8 @@ struct sb_ctx {
   int wavelet = 0;              // 0 Haar (reading A6), 1 Daubechies-4 (reading A32)
   float2* wbuf = nullptr;       // D4 coefficients [B][img]
   std::vector<float> samp_frac; // sampled fraction f of each problem's mask
-  void* lscr[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // Lambda build scratch (kept)
-  size_t lscr_bytes[5] = {0, 0, 0, 0, 0};
+  void* lscr[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // Lambda build scratch (kept)
+  size_t lscr_bytes[6] = {0, 0, 0, 0, 0, 0};
   float mu = 0, lam = 0, gam = 0;
   bool separable = false;
   int W = 8, G = 1;
@@ -838,13 +838,18 @@ static sb_status build_lambda(sb_ctx* c) {
   CK(lscratch(c, 1, &g, (size_t)c->B * c->img));
   CK(lscratch(c, 2, &rh, (size_t)a.nmask * c->img));
   CK(lscratch(c, 3, &bad, 1));
+  double* gpart = nullptr;  // split the coil pass over coil groups only for small batches
+  if (c->B * 32 < 2 * 148) CK(lscratch(c, 5, &gpart, (size_t)c->B * std::min(c->C, 16) * c->img));
   CK(cudaMemsetAsync(bad, 0, sizeof(int), c->st));
   a.tmp = tmp;
   a.g = g;
   a.rhat = rh;
   a.bad = bad;
+  a.gpart = gpart;
+  int extra = 0;
+  a.nextra = &extra;
   CK(launch_lambda_build(a, c->st));
-  c->launches += 8;
+  c->launches += 8 + extra;
   return finish_lambda(c, tmp, g, rh, bad, nullptr);
 }
 
@@ -876,10 +881,15 @@ static sb_status build_lambda3(sb_ctx* c) {
   CK(lscratch(c, 2, &rh, (size_t)a.nmask * pn));
   CK(lscratch(c, 4, &kc2, (size_t)c->B * pn));
   CK(lscratch(c, 3, &bad, 1));
+  double* gpart = nullptr;
+  CK(lscratch(c, 5, &gpart, (size_t)std::min(chunk, 16) * pn));
   CK(cudaMemsetAsync(bad, 0, sizeof(int), c->st));
   a.tmp = tmp;
   a.rhat = rh;
   a.bad = bad;
+  a.gpart = gpart;
+  int extra = 0;
+  a.nextra = &extra;
   for (int b = 0; b < c->B; ++b) {
     for (int p0 = 0; p0 < nplanes; p0 += chunk) {
       a.B = 1;
@@ -901,8 +911,9 @@ static sb_status build_lambda3(sb_ctx* c) {
   a.mask = c->pmask;
   a.d3 = 1;
   a.kc2 = kc2;
+  a.gpart = nullptr;
   CK(launch_lambda_tail(a, c->st));
-  c->launches += 6;
+  c->launches += 6 + extra;
   Lam3Args e;
   e.B = c->B;
   e.D0 = c->D0;
