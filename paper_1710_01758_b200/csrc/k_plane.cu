@@ -16,7 +16,14 @@
 //       X[kb + NYL*ka][kz] = sum_g W_G^{g ka} W_NY^{g kb} sum_y' x[G y' + g] W_NYL^{y' kb};
 // the pointwise step (mask r/N, or Lambda^{-1}) is applied there, and the inverse runs the
 // three stages backwards, writing the length-G inverse DFT back into the owners' tiles.
-// Two cluster barriers per transform pair; no global-memory round trip for the spectra.
+// No global-memory round trip for the spectra.  The exchange (XCH, the matvec and
+// preconditioner modes) is push-based: after its column DFT, CTA g stores rows kb of its tile
+// straight into CTA h's receive buffer with st.async (distributed shared memory), each store
+// counting its bytes on h's mbarrier; h waits for the full tile, transforms, and st.async-s the
+// results back into the owners' tiles against their second mbarrier.  Every wait is a data
+// dependency, so there is no cluster-wide barrier per coil (a cluster barrier costs ~0.4 us
+// plus a GPU-scope fence and an L1 invalidate).  ENCODE / ADJOINT keep the
+// pull exchange between two cluster barriers.
 //
 // Modes:
 //   KP_APPLY / KP_PCG / KP_RESID  q = mu sum_c conj(s_c) F^H(r F(s_c p))/.. + lambda L p + gamma p
@@ -91,14 +98,20 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
   constexpr bool MATVEC = (MODE == KP_APPLY || MODE == KP_PCG || MODE == KP_RESID);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* wb = reinterpret_cast<float2*>(smem_raw);  // P::WBS: row exchange / tile spectra
-  // the p (or x) tile exists only in the modes that multiply by it (matvec, encode)
-  constexpr bool HAS_PT = (MODE == KP_APPLY || MODE == KP_PCG || MODE == KP_RESID || MODE == KP_ENCODE);
+  // push exchange through st.async + mbarriers (see the header)
+  constexpr bool XCH = (G > 1) && (MATVEC || MODE == KP_PRECOND || MODE == KP_PRE2D);
+  // the p (or x) tile is kept in shared memory by the pull-exchange modes that multiply by it
+  // (encode); with XCH its slot holds the receive buffer and p is re-read from global (L2)
+  constexpr bool HAS_PT = !XCH && (MATVEC || MODE == KP_ENCODE);
   float2* pt = wb + P::WBS;                          // NYL x NZ: p (or x) tile, natural
-  float2* twz = pt + (HAS_PT ? NYL * NZ : 0);        // NZ
+  float2* recv = pt;                                 // XCH: NYL x NZ receive buffer
+  float2* twz = pt + ((HAS_PT || XCH) ? NYL * NZ : 0);  // NZ
   float2* twy = twz + NZ;                            // NY
   float2* sbuf = twy + NY;                           // P::PREF: [2][NYL x NZ] s_c tiles
   __shared__ double red[32];
   __shared__ int lastflag;
+  __shared__ __align__(8) uint64_t xbar[2];         // XCH: [0] receive buffer full, [1] tile returned
+  constexpr uint32_t XBYTES = (uint32_t)(NYL * NZ * sizeof(float2));
 
   const int g = blockIdx.x;  // cluster rank (cluster dims = (G,1,1), grid.x = G)
   const int xpl = blockIdx.y;
@@ -135,15 +148,33 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
     }
   }
   if (MATVEC && g == 0 && xpl == 0 && tid == 0 && a.L.cnt != nullptr) atomicAdd(&a.L.cnt->k1_problems, 1ull);
-  __syncthreads();
+  if constexpr (XCH) {
+    // both barriers armed for coil 0 before any peer can store (cluster barrier below)
+    if (tid == 0) {
+      mbar_init(&xbar[0], 1);
+      mbar_init(&xbar[1], 1);
+      fence_mbar_init();
+      mbar_expect_tx(&xbar[0], XBYTES);
+      mbar_expect_tx(&xbar[1], XBYTES);
+    }
+    cluster_sync_all();
+  } else {
+    __syncthreads();
+  }
 
   const float2* pold = pidx ? a.pbuf0 : a.pbuf1;
   float2* pnew = pidx ? a.pbuf1 : a.pbuf0;
   // global index of (local row rr, column z) of this plane
   auto gidx = [&](int rr, int z) { return poff + (size_t)(G * rr + g) * NZ + z; };
+  // p (or x) at local row rr, column z: the shared tile, or (XCH) this CTA's rows from global
+  auto pget = [&](int rr, int z) -> float2 {
+    if constexpr (HAS_PT) return pt[rr * NZ + z];
+    else if constexpr (MODE == KP_PCG) return pnew[gidx(rr, z)];
+    else return a.vin[gidx(rr, z)];
+  };
 
   // ---- prologue: p (or x / input) tile into shared memory; PCG p-update and deferred x
-  if constexpr (MATVEC || MODE == KP_ENCODE) {
+  if constexpr (HAS_PT || MODE == KP_PCG) {
     constexpr int E = (NYL * NZ + T - 1) / T;
     constexpr int CH = E < 8 ? E : 8;
     for (int c0 = 0; c0 < E; c0 += CH) {
@@ -177,7 +208,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
             }
             pnew[gi] = p;
           }
-          pt[e] = p;
+          if constexpr (HAS_PT) pt[e] = p;
         }
       }
     }
@@ -256,9 +287,9 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
             cp_async_wait_all();
             __syncthreads();
           }
-          v[n1] = cmul(sbuf[(c & 1) * NYL * NZ + r * NZ + z], pt[r * NZ + z]);
+          v[n1] = cmul(sbuf[(c & 1) * NYL * NZ + r * NZ + z], pget(r, z));
         } else {
-          v[n1] = cmul(a.sens[soff + (size_t)(G * r + g) * NZ + z], pt[r * NZ + z]);
+          v[n1] = cmul(a.sens[soff + (size_t)(G * r + g) * NZ + z], pget(r, z));
         }
       }
       fft_fwd<NZ, typename P::RLay>(v, wb, twz, j, r);
@@ -277,8 +308,21 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
 #pragma unroll
         for (int kb = 1; kb < NYL; ++kb)
           if (g > 0) colv[kb] = cmul(colv[kb], twy[g * kb]);
+        if constexpr (XCH) {
+          // rows [h KB, (h+1) KB) -> CTA h's receive buffer, slot (g KB + kbl, tid)
+          const uint32_t rl = smem_u32(recv) + (uint32_t)(((g * KB) * NZ + tid) * sizeof(float2));
+          const uint32_t bl = smem_u32(&xbar[0]);
 #pragma unroll
-        for (int kb = 0; kb < NYL; ++kb) wb[kb * NZ + tid] = colv[kb];
+          for (int h = 0; h < G; ++h) {
+            const uint32_t rr = mapa_u32(rl, h), bb = mapa_u32(bl, h);
+#pragma unroll
+            for (int kbl = 0; kbl < KB; ++kbl)
+              st_async_f2(rr + (uint32_t)(kbl * NZ * sizeof(float2)), colv[h * KB + kbl], bb);
+          }
+        } else {
+#pragma unroll
+          for (int kb = 0; kb < NYL; ++kb) wb[kb * NZ + tid] = colv[kb];
+        }
       }
     } else {
       // adjoint: the rows about to be overwritten by peers must be free (previous coil done)
@@ -290,9 +334,49 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) sv[n1] = a.sens[soff + (size_t)(G * r + g) * NZ + N2 * n1 + j];
     }
-    cl_sync<G>();
+    if constexpr (XCH) {
+      mbar_wait(&xbar[0], c & 1);  // all G x KB rows of every peer arrived
+      if (tid == 0 && c + 1 < ncoil) mbar_expect_tx(&xbar[0], XBYTES);
+    } else {
+      cl_sync<G>();
+    }
     // (3) cross-cluster DFT, pointwise operator, inverse cross-cluster DFT
-    if (tid < NZ) {
+    if (XCH && tid < NZ) {
+      const int kz = tid;
+      float2 wa[KB][G];
+#pragma unroll
+      for (int kbl = 0; kbl < KB; ++kbl)
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) wa[kbl][gg] = recv[(gg * KB + kbl) * NZ + kz];
+      const uint32_t wl = smem_u32(wb) + (uint32_t)((g * KB * NZ + kz) * sizeof(float2));
+      const uint32_t bl = smem_u32(&xbar[1]);
+#pragma unroll
+      for (int kbl = 0; kbl < KB; ++kbl) {
+        const int kb = g * KB + kbl;
+        float2* w = wa[kbl];
+        Dft<G, -1>::run(w);
+#pragma unroll
+        for (int ka = 0; ka < G; ++ka) {
+          const int ky = kb + NYL * ka;
+          float f;
+          if constexpr (MODE == KP_PRECOND || MODE == KP_PRE2D) {
+            f = a.lam_inv[boff + (size_t)xpl * PN + (size_t)ky * NZ + kz];
+          } else {
+            f = ((mbits >> (kbl * G + ka)) & 1u) ? a.scale : 0.f;
+          }
+          w[ka] = cscale(w[ka], f);
+        }
+        Dft<G, +1>::run(w);
+      }
+      // results for owner gg: its rows kb = g KB + kbl
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+        const uint32_t rr = mapa_u32(wl, gg), bb = mapa_u32(bl, gg);
+#pragma unroll
+        for (int kbl = 0; kbl < KB; ++kbl) st_async_f2(rr + (uint32_t)(kbl * NZ * sizeof(float2)), wa[kbl][gg], bb);
+      }
+    }
+    if (!XCH && tid < NZ) {
       const int kz = tid;
 #pragma unroll
       for (int kbl = 0; kbl < KB; ++kbl) {
@@ -339,7 +423,12 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
       cl_sync<G>();  // peers finished reading this tile before the next coil overwrites it
       continue;
     }
-    cl_sync<G>();
+    if constexpr (XCH) {
+      mbar_wait(&xbar[1], c & 1);  // every row of this tile is back from its transformer
+      if (tid == 0 && c + 1 < ncoil) mbar_expect_tx(&xbar[1], XBYTES);
+    } else {
+      cl_sync<G>();
+    }
     // (4) inverse local column DFT
     if (tid < NZ) {
 #pragma unroll
@@ -384,6 +473,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
     }
     __syncthreads();  // exchange reads done before the next coil writes wb
   }
+  if constexpr (XCH) cluster_sync_all();  // no CTA leaves while peers' st.async may target it
 
   if constexpr (MODE == KP_ADJOINT) {
 #pragma unroll
@@ -475,9 +565,9 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
 #pragma unroll
     for (int i = 0; i < CE; ++i) {
       const int z = N2 * (c0 + i) + j;
-      const float2 p = pt[r * NZ + z];
-      const float2 pl = pt[r * NZ + (z + NZ - 1) % NZ];
-      const float2 pr = pt[r * NZ + (z + 1) % NZ];
+      const float2 p = pget(r, z);
+      const float2 pl = pget(r, (z + NZ - 1) % NZ);
+      const float2 pr = pget(r, (z + 1) % NZ);
       float2 lp = make_float2(cdeg * p.x - pl.x - pr.x - nb[i][0].x - nb[i][1].x,
                               cdeg * p.y - pl.y - pr.y - nb[i][0].y - nb[i][1].y);
       if (D3) {
@@ -535,9 +625,11 @@ template <int NY, int NZ, int G, int MODE>
 static cudaError_t kp_launch(const KPArgs& a, cudaStream_t st) {
   using P = PlaneCfg<NY, NZ, G>;
   auto kern = kp_plane<NY, NZ, G, MODE>;
-  constexpr bool HAS_PT = (MODE == KP_APPLY || MODE == KP_PCG || MODE == KP_RESID || MODE == KP_ENCODE);
-  constexpr bool PF = P::PREF && (MODE == KP_APPLY || MODE == KP_PCG || MODE == KP_RESID || MODE == KP_ENCODE);
-  constexpr size_t smem = P::smem0 - (HAS_PT ? 0 : (size_t)P::NYL * NZ * sizeof(float2)) + (PF ? P::sbytes : 0);
+  constexpr bool MATVEC = (MODE == KP_APPLY || MODE == KP_PCG || MODE == KP_RESID);
+  constexpr bool XCH = (G > 1) && (MATVEC || MODE == KP_PRECOND || MODE == KP_PRE2D);
+  constexpr bool HAS_PT = !XCH && (MATVEC || MODE == KP_ENCODE);
+  constexpr bool PF = P::PREF && (MATVEC || MODE == KP_ENCODE);
+  constexpr size_t smem = P::smem0 - ((HAS_PT || XCH) ? 0 : (size_t)P::NYL * NZ * sizeof(float2)) + (PF ? P::sbytes : 0);
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
