@@ -329,6 +329,52 @@ __device__ __forceinline__ void fft_inv(V (&v)[Split<N>::N1], V* xch, const V* _
   Dft<N1, +1>::run(v);
 }
 
+// Transposed-table variants (row groups, j fastest across lanes): the forward twiddles come
+// from tf[k1 * N2 + j] = W_N^{j k1} and the inverse ones from ti[(q N2 + n2) N2 + j] =
+// W_N^{n2 (j + q N2)}, so the lanes of a warp read consecutive entries (the natural table
+// tw[j k1] is a strided gather with up to N2-way bank conflicts).
+template <int N, typename Lay, typename V>
+__device__ __forceinline__ void fft_fwd_t(V (&v)[Split<N>::N1], V* xch, const V* __restrict__ tf, int j, int line) {
+  constexpr int N1 = Split<N>::N1, N2 = Split<N>::N2;
+  Dft<N1, -1>::run(v);
+#pragma unroll
+  for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], tf[k1 * N2 + j]);
+#pragma unroll
+  for (int k1 = 0; k1 < N1; ++k1) xch[Lay::off(k1, j, line)] = v[k1];
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < N1 / N2; ++q) {
+    V u[N2];
+    const int k1 = j + q * N2;
+#pragma unroll
+    for (int n2 = 0; n2 < N2; ++n2) u[n2] = xch[Lay::off(k1, n2, line)];
+    Dft<N2, -1>::run(u);
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) v[q * N2 + k2] = u[k2];
+  }
+}
+template <int N, typename Lay, typename V>
+__device__ __forceinline__ void fft_inv_t(V (&v)[Split<N>::N1], V* xch, const V* __restrict__ ti, int j, int line) {
+  constexpr int N1 = Split<N>::N1, N2 = Split<N>::N2;
+#pragma unroll
+  for (int q = 0; q < N1 / N2; ++q) {
+    V u[N2];
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) u[k2] = v[q * N2 + k2];
+    Dft<N2, +1>::run(u);
+    const int k1 = j + q * N2;
+#pragma unroll
+    for (int n2 = 0; n2 < N2; ++n2) {
+      const V w = (n2 == 0) ? u[n2] : cmul_conjb(u[n2], ti[(q * N2 + n2) * N2 + j]);
+      xch[Lay::off(k1, n2, line)] = w;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k1 = 0; k1 < N1; ++k1) v[k1] = xch[Lay::off(k1, j, line)];
+  Dft<N1, +1>::run(v);
+}
+
 // Register-twiddle variants for square splits (N1 == N2): thread j's forward twiddles
 // W_N^{j k1} (k1 < N1) and inverse twiddles conj(W_N^{n2 j}) (n2 < N2) are the same N1 values,
 // loaded once per kernel into twr[m] = W_N^{j m} instead of from shared memory per transform.

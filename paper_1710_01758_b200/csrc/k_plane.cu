@@ -54,8 +54,12 @@ struct PlaneCfg {
   static_assert(NZ <= T, "column stage needs one thread per column");
   static_assert(NYL <= 32, "column DFT is register resident");
   using RLay = typename RowLayout<NZ, NYL>::L;
-  static constexpr int WBS = RowLayout<NZ, NYL>::size > NYL * NZ ? RowLayout<NZ, NYL>::size : NYL * NZ;
-  static constexpr size_t smem0 = (size_t)(WBS + NYL * NZ + NZ + NY) * sizeof(float2);
+  // row stride of the spectra tile in shared memory: == N2 (mod 32) elements, so the 32/N2 rows
+  // a warp touches in the row stage fall on distinct banks (no conflicts for 8-byte elements)
+  static constexpr int NZP = NZ + ((N2 - NZ) % 32 + 32) % 32;
+  static constexpr int WBS = RowLayout<NZ, NYL>::size > NYL * NZP ? RowLayout<NZ, NYL>::size : NYL * NZP;
+  // twiddles: forward table [k1][j] and inverse table [q][n2][j] (j fastest, conflict free) + NY
+  static constexpr size_t smem0 = (size_t)(WBS + NYL * NZ + 2 * NZ + NY) * sizeof(float2);
   // prefetch buffer for the next coil's s_c tile (cp.async) when it does not cost occupancy:
   // keep 2 CTAs/SM where they fit, else (already 1 CTA/SM) stay under the 227 KB limit
   // (double-buffered: s_c stays in shared memory for the conj multiply after the inverse)
@@ -93,7 +97,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
     kp_plane(const KPArgs a) {
   const bool D3 = a.d3 != 0;
   using P = PlaneCfg<NY, NZ, G>;
-  constexpr int NYL = P::NYL, KB = P::KB, N1 = P::N1, N2 = P::N2, T = P::T;
+  constexpr int NYL = P::NYL, KB = P::KB, N1 = P::N1, N2 = P::N2, T = P::T, NZP = P::NZP;
   constexpr int PN = NY * NZ;
   constexpr bool MATVEC = (MODE == KP_APPLY || MODE == KP_PCG || MODE == KP_RESID);
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -105,8 +109,8 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
   constexpr bool HAS_PT = !XCH && (MATVEC || MODE == KP_ENCODE);
   float2* pt = wb + P::WBS;                          // NYL x NZ: p (or x) tile, natural
   float2* recv = pt;                                 // XCH: NYL x NZ receive buffer
-  float2* twz = pt + ((HAS_PT || XCH) ? NYL * NZ : 0);  // NZ
-  float2* twy = twz + NZ;                            // NY
+  float2* twz = pt + ((HAS_PT || XCH) ? NYL * NZ : 0);  // 2 NZ: forward, inverse row twiddles
+  float2* twy = twz + 2 * NZ;                        // NY
   float2* sbuf = twy + NY;                           // P::PREF: [2][NYL x NZ] s_c tiles
   __shared__ double red[32];
   __shared__ int lastflag;
@@ -123,7 +127,11 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
   const size_t boff = (size_t)b * img;
   const size_t poff = boff + (size_t)xpl * PN;
 
-  for (int i = tid; i < NZ; i += T) twz[i] = a.tw_z[i];
+  for (int i = tid; i < NZ; i += T) {
+    const int k1 = i / N2, jj = i % N2, q = i / (N2 * N2), n2 = (i / N2) % N2;
+    twz[i] = a.tw_z[jj * k1];                 // W^{j k1}
+    twz[NZ + i] = a.tw_z[n2 * (jj + q * N2)];  // W^{n2 k1}, k1 = j + q N2
+  }
   for (int i = tid; i < NY; i += T) twy[i] = a.tw_y[i];
   pdl_trigger();
   pdl_wait();
@@ -292,18 +300,18 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
           v[n1] = cmul(a.sens[soff + (size_t)(G * r + g) * NZ + z], pget(r, z));
         }
       }
-      fft_fwd<NZ, typename P::RLay>(v, wb, twz, j, r);
+      fft_fwd_t<NZ, typename P::RLay>(v, wb, twz, j, r);
       if constexpr (PF) {  // every thread read sbuf before the barrier inside fft_fwd
         if (c + 1 < ncoil) prefetch_s(c + 1);
       }
       __syncthreads();
 #pragma unroll
-      for (int q = 0; q < N1; ++q) wb[r * NZ + specidx<NZ>(j, q)] = v[q];
+      for (int q = 0; q < N1; ++q) wb[r * NZP + specidx<NZ>(j, q)] = v[q];
       __syncthreads();
       // (2) local column DFT over y', twiddle W_NY^{g kb}
       if (tid < NZ) {
 #pragma unroll
-        for (int y = 0; y < NYL; ++y) colv[y] = wb[y * NZ + tid];
+        for (int y = 0; y < NYL; ++y) colv[y] = wb[y * NZP + tid];
         Dft<NYL, -1>::run(colv);
 #pragma unroll
         for (int kb = 1; kb < NYL; ++kb)
@@ -321,7 +329,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
           }
         } else {
 #pragma unroll
-          for (int kb = 0; kb < NYL; ++kb) wb[kb * NZ + tid] = colv[kb];
+          for (int kb = 0; kb < NYL; ++kb) wb[kb * NZP + tid] = colv[kb];
         }
       }
     } else {
@@ -348,7 +356,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
       for (int kbl = 0; kbl < KB; ++kbl)
 #pragma unroll
         for (int gg = 0; gg < G; ++gg) wa[kbl][gg] = recv[(gg * KB + kbl) * NZ + kz];
-      const uint32_t wl = smem_u32(wb) + (uint32_t)((g * KB * NZ + kz) * sizeof(float2));
+      const uint32_t wl = smem_u32(wb) + (uint32_t)((g * KB * NZP + kz) * sizeof(float2));
       const uint32_t bl = smem_u32(&xbar[1]);
 #pragma unroll
       for (int kbl = 0; kbl < KB; ++kbl) {
@@ -373,7 +381,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
       for (int gg = 0; gg < G; ++gg) {
         const uint32_t rr = mapa_u32(wl, gg), bb = mapa_u32(bl, gg);
 #pragma unroll
-        for (int kbl = 0; kbl < KB; ++kbl) st_async_f2(rr + (uint32_t)(kbl * NZ * sizeof(float2)), wa[kbl][gg], bb);
+        for (int kbl = 0; kbl < KB; ++kbl) st_async_f2(rr + (uint32_t)(kbl * NZP * sizeof(float2)), wa[kbl][gg], bb);
       }
     }
     if (!XCH && tid < NZ) {
@@ -392,7 +400,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
           }
         } else {
 #pragma unroll
-          for (int gg = 0; gg < G; ++gg) w[gg] = peer<G>(wb, gg)[kb * NZ + kz];
+          for (int gg = 0; gg < G; ++gg) w[gg] = peer<G>(wb, gg)[kb * NZP + kz];
           Dft<G, -1>::run(w);
 #pragma unroll
           for (int ka = 0; ka < G; ++ka) {
@@ -415,7 +423,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
         } else {
           Dft<G, +1>::run(w);
 #pragma unroll
-          for (int gg = 0; gg < G; ++gg) peer<G>(wb, gg)[kb * NZ + kz] = w[gg];
+          for (int gg = 0; gg < G; ++gg) peer<G>(wb, gg)[kb * NZP + kz] = w[gg];
         }
       }
     }
@@ -433,19 +441,19 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
     if (tid < NZ) {
 #pragma unroll
       for (int kb = 0; kb < NYL; ++kb) {
-        const float2 t = wb[kb * NZ + tid];
+        const float2 t = wb[kb * NZP + tid];
         colv[kb] = (g > 0 && kb > 0) ? cmul_conjb(t, twy[g * kb]) : t;
       }
       Dft<NYL, +1>::run(colv);
 #pragma unroll
-      for (int y = 0; y < NYL; ++y) wb[y * NZ + tid] = colv[y];
+      for (int y = 0; y < NYL; ++y) wb[y * NZP + tid] = colv[y];
     }
     __syncthreads();
     // (5) inverse row FFTs
 #pragma unroll
-    for (int q = 0; q < N1; ++q) v[q] = wb[r * NZ + specidx<NZ>(j, q)];
+    for (int q = 0; q < N1; ++q) v[q] = wb[r * NZP + specidx<NZ>(j, q)];
     __syncthreads();
-    fft_inv<NZ, typename P::RLay>(v, wb, twz, j, r);
+    fft_inv_t<NZ, typename P::RLay>(v, wb, twz + NZ, j, r);
     if constexpr (MODE == KP_PRECOND) {
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) a.tmp[gidx(r, N2 * n1 + j)] = v[n1];
