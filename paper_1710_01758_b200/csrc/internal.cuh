@@ -182,6 +182,14 @@ __device__ __forceinline__ void st_async_f2(uint32_t addr, float2 v, uint32_t ba
                "f"(v.x), "f"(v.y), "r"(bar)
                : "memory");
 }
+// bulk copy (async proxy) of `bytes` (multiple of 16, 16-byte aligned) from this CTA's shared
+// memory to a (possibly remote) CTA's shared memory, completion counted on that CTA's mbarrier
+__device__ __forceinline__ void bulk_s2s(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes, uint32_t bar_cluster) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst_cluster),
+               "r"(src_cta), "r"(bytes), "r"(bar_cluster)
+               : "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }

@@ -17,13 +17,15 @@
 // the pointwise step (mask r/N, or Lambda^{-1}) is applied there, and the inverse runs the
 // three stages backwards, writing the length-G inverse DFT back into the owners' tiles.
 // No global-memory round trip for the spectra.  The exchange (XCH, the matvec and
-// preconditioner modes) is push-based: after its column DFT, CTA g stores rows kb of its tile
-// straight into CTA h's receive buffer with st.async (distributed shared memory), each store
-// counting its bytes on h's mbarrier; h waits for the full tile, transforms, and st.async-s the
-// results back into the owners' tiles against their second mbarrier.  Every wait is a data
+// preconditioner modes) is push-based and runs on the bulk-copy (TMA) engine: after its column
+// DFT, CTA g copies rows [h KB, (h+1) KB) of its tile into CTA h's receive buffer with one
+// cp.async.bulk shared::cta -> shared::cluster per peer, completion counted in bytes on h's
+// mbarrier; h waits for the full buffer, transforms in place, and bulk-copies each owner's rows
+// back into the owner's tile against the owner's second mbarrier.  Every wait is a data
 // dependency, so there is no cluster-wide barrier per coil (a cluster barrier costs ~0.4 us
-// plus a GPU-scope fence and an L1 invalidate).  ENCODE / ADJOINT keep the
-// pull exchange between two cluster barriers.
+// plus a GPU-scope fence and an L1 invalidate), and the threads issue no
+// per-element remote stores.  ENCODE / ADJOINT keep the pull exchange between two cluster
+// barriers.
 //
 // Modes:
 //   KP_APPLY / KP_PCG / KP_RESID  q = mu sum_c conj(s_c) F^H(r F(s_c p))/.. + lambda L p + gamma p
@@ -59,7 +61,8 @@ struct PlaneCfg {
   static constexpr int NZP = NZ + ((N2 - NZ) % 32 + 32) % 32;
   static constexpr int WBS = RowLayout<NZ, NYL>::size > NYL * NZP ? RowLayout<NZ, NYL>::size : NYL * NZP;
   // twiddles: forward table [k1][j] and inverse table [q][n2][j] (j fastest, conflict free) + NY
-  static constexpr size_t smem0 = (size_t)(WBS + NYL * NZ + 2 * NZ + NY) * sizeof(float2);
+  static constexpr int TS = NYL * NZP;  // p tile / receive buffer slot
+  static constexpr size_t smem0 = (size_t)(WBS + TS + 2 * NZ + NY) * sizeof(float2);
   // prefetch buffer for the next coil's s_c tile (cp.async) when it does not cost occupancy:
   // keep 2 CTAs/SM where they fit, else (already 1 CTA/SM) stay under the 227 KB limit
   // (double-buffered: s_c stays in shared memory for the conj multiply after the inverse)
@@ -102,20 +105,21 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
   constexpr bool MATVEC = (MODE == KP_APPLY || MODE == KP_PCG || MODE == KP_RESID);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* wb = reinterpret_cast<float2*>(smem_raw);  // P::WBS: row exchange / tile spectra
-  // push exchange through st.async + mbarriers (see the header)
+  // push exchange through bulk copies + mbarriers (see the header)
   constexpr bool XCH = (G > 1) && (MATVEC || MODE == KP_PRECOND || MODE == KP_PRE2D);
   // the p (or x) tile is kept in shared memory by the pull-exchange modes that multiply by it
   // (encode); with XCH its slot holds the receive buffer and p is re-read from global (L2)
   constexpr bool HAS_PT = !XCH && (MATVEC || MODE == KP_ENCODE);
   float2* pt = wb + P::WBS;                          // NYL x NZ: p (or x) tile, natural
   float2* recv = pt;                                 // XCH: NYL x NZ receive buffer
-  float2* twz = pt + ((HAS_PT || XCH) ? NYL * NZ : 0);  // 2 NZ: forward, inverse row twiddles
+  float2* twz = pt + ((HAS_PT || XCH) ? P::TS : 0);  // 2 NZ: forward, inverse row twiddles
   float2* twy = twz + 2 * NZ;                        // NY
   float2* sbuf = twy + NY;                           // P::PREF: [2][NYL x NZ] s_c tiles
   __shared__ double red[32];
   __shared__ int lastflag;
   __shared__ __align__(8) uint64_t xbar[2];         // XCH: [0] receive buffer full, [1] tile returned
-  constexpr uint32_t XBYTES = (uint32_t)(NYL * NZ * sizeof(float2));
+  constexpr uint32_t XBYTES = (uint32_t)(NYL * NZP * sizeof(float2));
+  constexpr uint32_t XROWS = (uint32_t)(KB * NZP * sizeof(float2));  // one bulk copy: KB tile rows
 
   const int g = blockIdx.x;  // cluster rank (cluster dims = (G,1,1), grid.x = G)
   const int xpl = blockIdx.y;
@@ -316,20 +320,17 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
 #pragma unroll
         for (int kb = 1; kb < NYL; ++kb)
           if (g > 0) colv[kb] = cmul(colv[kb], twy[g * kb]);
-        if constexpr (XCH) {
-          // rows [h KB, (h+1) KB) -> CTA h's receive buffer, slot (g KB + kbl, tid)
-          const uint32_t rl = smem_u32(recv) + (uint32_t)(((g * KB) * NZ + tid) * sizeof(float2));
-          const uint32_t bl = smem_u32(&xbar[0]);
 #pragma unroll
-          for (int h = 0; h < G; ++h) {
-            const uint32_t rr = mapa_u32(rl, h), bb = mapa_u32(bl, h);
-#pragma unroll
-            for (int kbl = 0; kbl < KB; ++kbl)
-              st_async_f2(rr + (uint32_t)(kbl * NZ * sizeof(float2)), colv[h * KB + kbl], bb);
-          }
-        } else {
-#pragma unroll
-          for (int kb = 0; kb < NYL; ++kb) wb[kb * NZP + tid] = colv[kb];
+        for (int kb = 0; kb < NYL; ++kb) wb[kb * NZP + tid] = colv[kb];
+      }
+      if constexpr (XCH) {
+        // rows [h KB, (h+1) KB) -> CTA h's receive buffer rows [g KB, (g+1) KB): G bulk copies
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+          const uint32_t dst = smem_u32(recv + g * KB * NZP), bar = smem_u32(&xbar[0]);
+#pragma unroll 1
+          for (int h = 0; h < G; ++h) bulk_s2s(mapa_u32(dst, h), smem_u32(wb + h * KB * NZP), XROWS, mapa_u32(bar, h));
         }
       }
     } else {
@@ -355,9 +356,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
 #pragma unroll
       for (int kbl = 0; kbl < KB; ++kbl)
 #pragma unroll
-        for (int gg = 0; gg < G; ++gg) wa[kbl][gg] = recv[(gg * KB + kbl) * NZ + kz];
-      const uint32_t wl = smem_u32(wb) + (uint32_t)((g * KB * NZP + kz) * sizeof(float2));
-      const uint32_t bl = smem_u32(&xbar[1]);
+        for (int gg = 0; gg < G; ++gg) wa[kbl][gg] = recv[(gg * KB + kbl) * NZP + kz];
 #pragma unroll
       for (int kbl = 0; kbl < KB; ++kbl) {
         const int kb = g * KB + kbl;
@@ -376,12 +375,20 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
         }
         Dft<G, +1>::run(w);
       }
-      // results for owner gg: its rows kb = g KB + kbl
+      // results in place: rows (gg KB + kbl) of the receive buffer belong to owner gg
 #pragma unroll
-      for (int gg = 0; gg < G; ++gg) {
-        const uint32_t rr = mapa_u32(wl, gg), bb = mapa_u32(bl, gg);
+      for (int kbl = 0; kbl < KB; ++kbl)
 #pragma unroll
-        for (int kbl = 0; kbl < KB; ++kbl) st_async_f2(rr + (uint32_t)(kbl * NZP * sizeof(float2)), wa[kbl][gg], bb);
+        for (int gg = 0; gg < G; ++gg) recv[(gg * KB + kbl) * NZP + kz] = wa[kbl][gg];
+    }
+    if constexpr (XCH) {
+      // owner gg's rows [g KB, (g+1) KB) go back into its tile: G bulk copies
+      fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) {
+        const uint32_t dst = smem_u32(wb + g * KB * NZP), bar = smem_u32(&xbar[1]);
+#pragma unroll 1
+        for (int gg = 0; gg < G; ++gg) bulk_s2s(mapa_u32(dst, gg), smem_u32(recv + gg * KB * NZP), XROWS, mapa_u32(bar, gg));
       }
     }
     if (!XCH && tid < NZ) {
@@ -481,7 +488,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
     }
     __syncthreads();  // exchange reads done before the next coil writes wb
   }
-  if constexpr (XCH) cluster_sync_all();  // no CTA leaves while peers' st.async may target it
+  if constexpr (XCH) cluster_sync_all();  // no CTA leaves while bulk copies may still read its tile
 
   if constexpr (MODE == KP_ADJOINT) {
 #pragma unroll
@@ -637,7 +644,7 @@ static cudaError_t kp_launch(const KPArgs& a, cudaStream_t st) {
   constexpr bool XCH = (G > 1) && (MATVEC || MODE == KP_PRECOND || MODE == KP_PRE2D);
   constexpr bool HAS_PT = !XCH && (MATVEC || MODE == KP_ENCODE);
   constexpr bool PF = P::PREF && (MATVEC || MODE == KP_ENCODE);
-  constexpr size_t smem = P::smem0 - ((HAS_PT || XCH) ? 0 : (size_t)P::NYL * NZ * sizeof(float2)) + (PF ? P::sbytes : 0);
+  constexpr size_t smem = P::smem0 - ((HAS_PT || XCH) ? 0 : (size_t)P::TS * sizeof(float2)) + (PF ? P::sbytes : 0);
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
