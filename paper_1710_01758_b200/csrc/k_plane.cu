@@ -63,11 +63,12 @@ struct PlaneCfg {
   // twiddles: forward table [k1][j] and inverse table [q][n2][j] (j fastest, conflict free) + NY
   static constexpr int TS = NYL * NZP;  // p tile / receive buffer slot
   static constexpr size_t smem0 = (size_t)(WBS + TS + 2 * NZ + NY) * sizeof(float2);
-  // prefetch buffer for the next coil's s_c tile (cp.async) when it does not cost occupancy:
-  // keep 2 CTAs/SM where they fit, else (already 1 CTA/SM) stay under the 227 KB limit
-  // (double-buffered: s_c stays in shared memory for the conj multiply after the inverse)
+  // prefetch buffer for the next coil's s_c tile (cp.async), double-buffered (s_c stays in
+  // shared memory for the conj multiply after the inverse).  Only where the kernel is already
+  // at 1 CTA/SM: elsewhere occupancy wins (config 4's 256x128 planes: no prefetch + 4 CTAs/SM
+  // at <= 128 registers is 915 us per K1P launch vs 1059 us with the prefetch at 3 CTAs/SM)
   static constexpr size_t sbytes = 2 * (size_t)NYL * NZ * sizeof(float2);
-  static constexpr bool PREF = (smem0 + sbytes <= 110 * 1024) || (smem0 > 113 * 1024 && smem0 + sbytes <= 220 * 1024);
+  static constexpr bool PREF = smem0 > 113 * 1024 && smem0 + sbytes <= 220 * 1024;
   static constexpr size_t smem = smem0 + (PREF ? sbytes : 0);
 };
 
@@ -96,7 +97,7 @@ __device__ __forceinline__ float2* peer(float2* p, int rank) {
 }
 
 template <int NY, int NZ, int G, int MODE>
-__global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T <= 128 ? 3 : (PlaneCfg<NY, NZ, G>::T <= 256 ? 2 : 1))
+__global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T <= 128 ? 4 : (PlaneCfg<NY, NZ, G>::T <= 256 ? 2 : 1))
     kp_plane(const KPArgs a) {
   const bool D3 = a.d3 != 0;
   using P = PlaneCfg<NY, NZ, G>;
