@@ -344,6 +344,19 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) sv[n1] = a.sens[soff + (size_t)(G * r + g) * NZ + N2 * n1 + j];
     }
+    // the preconditioner's Lambda^{-1} values of this CTA's spectral rows, loaded before the
+    // exchange wait so their latency hides behind it
+    constexpr bool LAMF = XCH && (MODE == KP_PRECOND || MODE == KP_PRE2D);
+    float lf[LAMF ? KB : 1][LAMF ? G : 1];
+    if constexpr (LAMF) {
+      if (tid < NZ) {
+#pragma unroll
+        for (int kbl = 0; kbl < KB; ++kbl)
+#pragma unroll
+          for (int ka = 0; ka < G; ++ka)
+            lf[kbl][ka] = a.lam_inv[boff + (size_t)xpl * PN + (size_t)(g * KB + kbl + NYL * ka) * NZ + tid];
+      }
+    }
     if constexpr (XCH) {
       mbar_wait(&xbar[0], c & 1);  // all G x KB rows of every peer arrived
       if (tid == 0 && c + 1 < ncoil) mbar_expect_tx(&xbar[0], XBYTES);
@@ -367,12 +380,13 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
         for (int ka = 0; ka < G; ++ka) {
           const int ky = kb + NYL * ka;
           float f;
-          if constexpr (MODE == KP_PRECOND || MODE == KP_PRE2D) {
-            f = a.lam_inv[boff + (size_t)xpl * PN + (size_t)ky * NZ + kz];
+          if constexpr (LAMF) {
+            f = lf[kbl][ka];
           } else {
             f = ((mbits >> (kbl * G + ka)) & 1u) ? a.scale : 0.f;
           }
           w[ka] = cscale(w[ka], f);
+          (void)ky;
         }
         Dft<G, +1>::run(w);
       }
