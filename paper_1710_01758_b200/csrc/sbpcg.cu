@@ -1198,6 +1198,10 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   // K1 configuration: W columns per tile; G-CTA clusters split the coils when the
   // problem alone would not fill the 148 SMs.
   c->W = k1_default_W(c->M, c->N);
+  if (const char* we = getenv("SBPCG_K1_W")) {  // debugging override of the tile width (4 or 8)
+    const int w = atoi(we);
+    if ((w == 4 || w == 8) && c->N % w == 0) c->W = w;
+  }
   c->G = 1;
   const int tiles = c->N / c->W;
   for (int g = 2; g <= 8; g *= 2)
