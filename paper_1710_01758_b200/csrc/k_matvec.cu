@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
   const bool need_old = (MODE == K1_PCG) && !first;
   // one pass over the tile: p_k into shared memory, and for this CTA's own rows (non-halo
   // columns) also p_k -> pnew and the deferred x += alpha_{k-1} p_{k-1} (p_{k-1} is read once)
+#pragma unroll 1
   for (int c0 = 0; c0 < PE; c0 += CH) {
     float2 zz[CH], po[CH], xv[CH];
     bool own[CH];
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
   constexpr int EE = (M * W + NT - 1) / NT;  // upper bound of epilogue elements per thread
   constexpr int CH3 = EE < 8 ? EE : 8;
   const int nep = rows_per * W;
+#pragma unroll 1
   for (int c0 = 0; c0 < EE; c0 += CH3) {
     float2 lb[CH3], lu[CH3], lu1[CH3], lr[CH3];
     if constexpr (MODE == K1_RESID) {
@@ -231,12 +233,24 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
       const int e = (c0 + i) * NT + tid;
       if (!(c0 + i < EE && e < nep)) continue;
       const int row = r0 + e / W, cc = e % W;
+      // fixed-order sum over the cluster's partials (rank 0 first), four DSMEM loads in flight
       float2 av = make_float2(0.f, 0.f);
-      for (int gg = 0; gg < G; ++gg) {
-        const float2* src = (gg == g) ? accb : cluster.map_shared_rank(accb, gg);
-        const float2 t = src[row * W + cc];
-        av.x += t.x;
-        av.y += t.y;
+#pragma unroll 1
+      for (int g0 = 0; g0 < G; g0 += 4) {
+        float2 t[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int gg = g0 + k;
+          t[k] = make_float2(0.f, 0.f);
+          if (gg < G) t[k] = ((gg == g) ? accb : cluster.map_shared_rank(accb, gg))[row * W + cc];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (g0 + k < G) {
+            av.x += t[k].x;
+            av.y += t[k].y;
+          }
+        }
       }
       const float2 p = pt[row * PW + cc + 1];
       const float2 pu = pt[((row + M - 1) % M) * PW + cc + 1];
