@@ -190,6 +190,13 @@ __device__ __forceinline__ void bulk_s2s(uint32_t dst_cluster, uint32_t src_cta,
                "r"(src_cta), "r"(bytes), "r"(bar_cluster)
                : "memory");
 }
+// split cluster barrier without memory ordering (the data exchanged by bulk copies is ordered by
+// the mbarriers; mbarrier initialisation is released by fence.mbarrier_init): no GPU-scope
+// fence, no L1 invalidate
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }

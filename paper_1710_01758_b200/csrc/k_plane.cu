@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
   }
   if (MATVEC && g == 0 && xpl == 0 && tid == 0 && a.L.cnt != nullptr) atomicAdd(&a.L.cnt->k1_problems, 1ull);
   if constexpr (XCH) {
-    // both barriers armed for coil 0 before any peer can store (cluster barrier below)
+    // both barriers armed for coil 0 before any peer can copy: a split cluster barrier whose
+    // wait sits just before the first copy, so its latency hides behind coil 0's row stage
     if (tid == 0) {
       mbar_init(&xbar[0], 1);
       mbar_init(&xbar[1], 1);
@@ -170,7 +171,8 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
       mbar_expect_tx(&xbar[0], XBYTES);
       mbar_expect_tx(&xbar[1], XBYTES);
     }
-    cluster_sync_all();
+    __syncthreads();
+    cluster_arrive_relaxed();
   } else {
     __syncthreads();
   }
@@ -327,6 +329,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
       if constexpr (XCH) {
         // rows [h KB, (h+1) KB) -> CTA h's receive buffer rows [g KB, (g+1) KB): G bulk copies
         fence_proxy_async();
+        if (c == 0) cluster_wait();  // every peer's barriers are initialised
         __syncthreads();
         if (tid == 0) {
           const uint32_t dst = smem_u32(recv + g * KB * NZP), bar = smem_u32(&xbar[0]);
@@ -503,7 +506,10 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
     }
     __syncthreads();  // exchange reads done before the next coil writes wb
   }
-  if constexpr (XCH) cluster_sync_all();  // no CTA leaves while bulk copies may still read its tile
+  if constexpr (XCH) {  // no CTA leaves while bulk copies may still read its tile
+    cluster_arrive_relaxed();
+    cluster_wait();
+  }
 
   if constexpr (MODE == KP_ADJOINT) {
 #pragma unroll
