@@ -23,8 +23,10 @@ __device__ __forceinline__ float2 shrinkc(float2 z, float t) {
   return make_float2(z.x * s, z.y * s);
 }
 
-// TT = max tile edge: 32, or 16 when a 32-tile grid would leave SMs idle (one 256^2 slice)
-template <int TT>
+// TT = max tile edge: 32, or 16 when a 32-tile grid would leave SMs idle (one 256^2 slice).
+// FIX: both image edges are multiples of TT, so the tile is TT x TT at compile time and every
+// index division below is a shift or a constant-divisor multiply (the kernel is issue bound).
+template <int TT, bool FIX>
 __global__ void __launch_bounds__(256) k_sb_update(const SbArgs a) {
   __shared__ float2 xs[TT + 2][TT + 2];
   __shared__ float2 vx[TT + 1][TT];
@@ -32,10 +34,15 @@ __global__ void __launch_bounds__(256) k_sb_update(const SbArgs a) {
   __shared__ float2 wa[TT][TT];
   __shared__ float2 wv[TT][TT];
   const int M = a.M, N = a.N, L = a.levels;
-  const int TH = M < TT ? M : TT, TW = N < TT ? N : TT;
+  const int TH = FIX ? TT : (M < TT ? M : TT), TW = FIX ? TT : (N < TT ? N : TT);
+  constexpr int LTT = TT == 32 ? 5 : 4;  // log2(TT)
+  // e / (TW >> lv) and e % (TW >> lv) for the Haar groups (TW a power of two when FIX)
+  auto gdiv = [&](int e, int lv) { return FIX ? (e >> (LTT - lv)) : e / (TW >> lv); };
+  auto gmod = [&](int e, int lv) { return FIX ? (e & ((TT >> lv) - 1)) : e % (TW >> lv); };
   const int i0 = blockIdx.x * TH, j0 = blockIdx.y * TW, b = blockIdx.z;
   const size_t img = (size_t)M * N, boff = (size_t)b * img;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x;
+  constexpr int nt = 256;  // launch_sb_update's block size
   const bool do_tv = a.lam != 0.f, do_w = a.gam != 0.f;
   const float tl = do_tv ? 1.f / a.lam : 0.f, tg = do_w ? 1.f / a.gam : 0.f;
   pdl_trigger();
@@ -97,8 +104,8 @@ __global__ void __launch_bounds__(256) k_sb_update(const SbArgs a) {
         const int e = base + tid;
         const bool act = e < h0 * h1;
         if (act) {
-          ga = e / h1;
-          gb = e % h1;
+          ga = gdiv(e, lv);
+          gb = gmod(e, lv);
           const float2 p = wa[2 * ga][2 * gb], q = wa[2 * ga][2 * gb + 1];
           const float2 r = wa[2 * ga + 1][2 * gb], s = wa[2 * ga + 1][2 * gb + 1];
           const float2 pr = make_float2(p.x + r.x, p.y + r.y), mr = make_float2(p.x - r.x, p.y - r.y);
@@ -159,8 +166,8 @@ __global__ void __launch_bounds__(256) k_sb_update(const SbArgs a) {
         float2 p, q, r, s;
         int ga = 0, gb = 0;
         if (act) {
-          ga = e / h1;
-          gb = e % h1;
+          ga = gdiv(e, lv);
+          gb = gmod(e, lv);
           const float2 LL = wv[ga][gb], LH = wv[ga][h1 + gb], HL = wv[h0 + ga][gb],
                        HH = wv[h0 + ga][h1 + gb];
           p = make_float2(0.5f * (LL.x + LH.x + HL.x + HH.x), 0.5f * (LL.y + LH.y + HL.y + HH.y));
@@ -202,8 +209,10 @@ cudaError_t launch_sb_update(const SbArgs& a, cudaStream_t st) {
   if (a.M % TH || a.N % TW || (TH % (1 << a.levels)) || (TW % (1 << a.levels))) return cudaErrorInvalidValue;
   const bool small = (int64_t)(a.M / TH) * (a.N / TW) * a.B < 2 * 148;
   if (small && a.M >= 16 && a.N >= 16 && a.M % 16 == 0 && a.N % 16 == 0 && (16 % (1 << a.levels)) == 0)
-    return launch_ex(k_sb_update<16>, dim3(a.M / 16, a.N / 16, a.B), dim3(256), 0, st, 0, a);
-  return launch_ex(k_sb_update<SBT>, dim3(a.M / TH, a.N / TW, a.B), dim3(256), 0, st, 0, a);
+    return launch_ex(k_sb_update<16, true>, dim3(a.M / 16, a.N / 16, a.B), dim3(256), 0, st, 0, a);
+  if (a.M % SBT == 0 && a.N % SBT == 0)
+    return launch_ex(k_sb_update<SBT, true>, dim3(a.M / SBT, a.N / SBT, a.B), dim3(256), 0, st, 0, a);
+  return launch_ex(k_sb_update<SBT, false>, dim3(a.M / TH, a.N / TW, a.B), dim3(256), 0, st, 0, a);
 }
 
 }  // namespace sbk
