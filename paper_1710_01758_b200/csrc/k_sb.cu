@@ -224,6 +224,8 @@ namespace sbk {
 
 constexpr int S3 = 8;
 
+// FIX: every edge is a multiple of S3, so the tile is S3^3 at compile time (index math as shifts)
+template <bool FIX>
 __global__ void __launch_bounds__(256) k_sb_update3(const SbArgs a) {
   __shared__ float2 xs[S3 + 2][S3 + 2][S3 + 2];
   __shared__ float2 v0[S3 + 1][S3][S3];
@@ -232,20 +234,25 @@ __global__ void __launch_bounds__(256) k_sb_update3(const SbArgs a) {
   __shared__ float2 wa[S3][S3][S3];
   __shared__ float2 wv[S3][S3][S3];
   const int D0 = a.M, D1 = a.N, D2 = a.D2, L = a.levels;
-  const int T0 = D0 < S3 ? D0 : S3, T1 = D1 < S3 ? D1 : S3, T2 = D2 < S3 ? D2 : S3;
+  const int T0 = FIX ? S3 : (D0 < S3 ? D0 : S3), T1 = FIX ? S3 : (D1 < S3 ? D1 : S3),
+            T2 = FIX ? S3 : (D2 < S3 ? D2 : S3);
   const int n1t = D1 / T1, n2t = D2 / T2;
   const int t = blockIdx.x;
   const int i0 = (t / (n1t * n2t)) * T0, j0 = ((t / n2t) % n1t) * T1, k0 = (t % n2t) * T2;
   const int b = blockIdx.y;
   const size_t img = (size_t)D0 * D1 * D2, boff = (size_t)b * img;
   auto G = [&](int i, int j, int k) { return boff + ((size_t)i * D1 + j) * D2 + k; };
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x;
+  constexpr int nt = 256;  // launch_sb_update3's block size
   const bool do_tv = a.lam != 0.f, do_w = a.gam != 0.f;
   const float tl = do_tv ? 1.f / a.lam : 0.f, tg = do_w ? 1.f / a.gam : 0.f;
   pdl_trigger();
   pdl_wait();
 
   const int X0 = T0 + 2, X1 = T1 + 2, X2 = T2 + 2;
+  // x / d, x % d for the Haar pair indices (d a power of two when FIX)
+  auto dv = [&](int x, int d) { return FIX ? (x >> (31 - __clz(d))) : x / d; };
+  auto md = [&](int x, int d) { return FIX ? (x & (d - 1)) : x % d; };
   for (int e = tid; e < X0 * X1 * X2; e += nt) {
     const int u = e / (X1 * X2), v = (e / X2) % X1, w = e % X2;
     xs[u][v][w] = a.x[G((i0 + u - 1 + D0) % D0, (j0 + v - 1 + D1) % D1, (k0 + w - 1 + D2) % D2)];
@@ -313,9 +320,9 @@ __global__ void __launch_bounds__(256) k_sb_update3(const SbArgs a) {
         int p0 = 0, p1 = 0, p2 = 0;
         const bool act = tid < n;  // <= 256 pairs at an 8^3 tile
         if (act) {
-          if (ax == 0) { p0 = tid / (e1 * e2); p1 = (tid / e2) % e1; p2 = tid % e2; }
-          else if (ax == 1) { p0 = tid / ((e1 / 2) * e2); p1 = (tid / e2) % (e1 / 2); p2 = tid % e2; }
-          else { p0 = tid / (e1 * (e2 / 2)); p1 = (tid / (e2 / 2)) % e1; p2 = tid % (e2 / 2); }
+          if (ax == 0) { p0 = dv(tid, e1 * e2); p1 = md(dv(tid, e2), e1); p2 = md(tid, e2); }
+          else if (ax == 1) { p0 = dv(tid, (e1 / 2) * e2); p1 = md(dv(tid, e2), e1 / 2); p2 = md(tid, e2); }
+          else { p0 = dv(tid, e1 * (e2 / 2)); p1 = md(dv(tid, e2 / 2), e1); p2 = md(tid, e2 / 2); }
           float2 ev, od;
           if (ax == 0) { ev = wa[2 * p0][p1][p2]; od = wa[2 * p0 + 1][p1][p2]; }
           else if (ax == 1) { ev = wa[p0][2 * p1][p2]; od = wa[p0][2 * p1 + 1][p2]; }
@@ -378,9 +385,9 @@ __global__ void __launch_bounds__(256) k_sb_update3(const SbArgs a) {
         const bool act = tid < n;
         if (act) {
           float2 lo, hi;
-          if (ax == 0) { p0 = tid / (e1 * e2); p1 = (tid / e2) % e1; p2 = tid % e2; lo = wv[p0][p1][p2]; hi = wv[e0 / 2 + p0][p1][p2]; }
-          else if (ax == 1) { p0 = tid / ((e1 / 2) * e2); p1 = (tid / e2) % (e1 / 2); p2 = tid % e2; lo = wv[p0][p1][p2]; hi = wv[p0][e1 / 2 + p1][p2]; }
-          else { p0 = tid / (e1 * (e2 / 2)); p1 = (tid / (e2 / 2)) % e1; p2 = tid % (e2 / 2); lo = wv[p0][p1][p2]; hi = wv[p0][p1][e2 / 2 + p2]; }
+          if (ax == 0) { p0 = dv(tid, e1 * e2); p1 = md(dv(tid, e2), e1); p2 = md(tid, e2); lo = wv[p0][p1][p2]; hi = wv[e0 / 2 + p0][p1][p2]; }
+          else if (ax == 1) { p0 = dv(tid, (e1 / 2) * e2); p1 = md(dv(tid, e2), e1 / 2); p2 = md(tid, e2); lo = wv[p0][p1][p2]; hi = wv[p0][e1 / 2 + p1][p2]; }
+          else { p0 = dv(tid, e1 * (e2 / 2)); p1 = md(dv(tid, e2 / 2), e1); p2 = md(tid, e2 / 2); lo = wv[p0][p1][p2]; hi = wv[p0][p1][e2 / 2 + p2]; }
           ev = make_float2(h * (lo.x + hi.x), h * (lo.y + hi.y));
           od = make_float2(h * (lo.x - hi.x), h * (lo.y - hi.y));
         }
@@ -418,7 +425,9 @@ cudaError_t launch_sb_update3(const SbArgs& a, cudaStream_t st) {
   const int q = 1 << a.levels;
   if (a.M % T0 || a.N % T1 || a.D2 % T2 || T0 % q || T1 % q || T2 % q) return cudaErrorInvalidValue;
   const int tiles = (a.M / T0) * (a.N / T1) * (a.D2 / T2);
-  return launch_ex(k_sb_update3, dim3(tiles, a.B), dim3(256), 0, st, 0, a);
+  if (a.M % S3 == 0 && a.N % S3 == 0 && a.D2 % S3 == 0)
+    return launch_ex(k_sb_update3<true>, dim3(tiles, a.B), dim3(256), 0, st, 0, a);
+  return launch_ex(k_sb_update3<false>, dim3(tiles, a.B), dim3(256), 0, st, 0, a);
 }
 
 }  // namespace sbk
