@@ -40,8 +40,14 @@ __device__ __forceinline__ bool slice_active(const PassArgs& a, int b) {
 }
 
 // ------------------------------------------------------------------ column passes
+// M = 192 (24 values per thread) is capped at 128 registers for 16 warps per SM: uncapped the
+// compiler takes ~250 and the 3D d0 passes run at 8 warps per SM (config 5's K2c: 56 -> 47 us)
+template <int M, int NT>
+struct ColMinBlocks {
+  static constexpr int value = (M == 192 && 512 / NT > 0) ? 512 / NT : 0;  // 0: unconstrained
+};
 template <int M, int W_, int KIND>
-__global__ void __launch_bounds__(ColCfg<M, W_>::NT) k_col(const PassArgs a) {
+__global__ void __launch_bounds__(ColCfg<M, W_>::NT, (ColMinBlocks<M, ColCfg<M, W_>::NT>::value)) k_col(const PassArgs a) {
   using C = ColCfg<M, W_>;
   constexpr int N1 = C::N1, W = C::W, NT = C::NT;
   __shared__ __align__(16) float2 xch[C::XS];
@@ -452,6 +458,13 @@ static cudaError_t launch_col_t(const PassArgs& a, cudaStream_t st) {
   if (WS < 8 && (a.N / 8) * nimg < kFill) {
     return launch_ex(k_col<M, (WS < 8 ? WS : 8), KIND>, dim3(a.N / WS, nimg), dim3(ColCfg<M, (WS < 8 ? WS : 8)>::NT),
                      0, st, 0, a);
+  }
+  if constexpr (M == 192) {
+    // wide tiles for large grids: 16 columns = one 128-byte line per row (the 3D d0 passes
+    // stride by a whole plane between rows, so 8-column tiles fetch half lines; measured
+    // slower for the 2D 256-row passes of config 3)
+    if (a.N % 16 == 0 && (a.N / 16) * nimg >= 4 * kFill)
+      return launch_ex(k_col<M, 16, KIND>, dim3(a.N / 16, nimg), dim3(ColCfg<M, 16>::NT), 0, st, 0, a);
   }
   return launch_ex(k_col<M, 8, KIND>, dim3(a.N / 8, nimg), dim3(ColCfg<M, 8>::NT), 0, st, 0, a);
 }
