@@ -39,9 +39,10 @@
 extern "C" {
 #endif
 
-#define SBPCG_ABI_VERSION 1
+#define SBPCG_ABI_VERSION 2
 
 typedef struct sb_ctx sb_ctx;
+typedef struct sb_comm sb_comm;  /* NCCL communicator of the coil-sharded mode (see below) */
 typedef struct { float re, im; } sb_c64;
 
 typedef enum {
@@ -57,7 +58,9 @@ typedef enum {
   SB_E_INDEFINITE = 7,       /* <p, A p> <= 0 (A must be HPD)            */
   SB_E_CUDA = 8,             /* CUDA runtime error (sticky)                            */
   SB_E_NOMEM = 9,            /* device allocation failed                               */
-  SB_E_COMM = 10             /* reserved: coil-sharded communicator errors             */
+  SB_E_COMM = 10             /* coil-sharded mode: NCCL could not be loaded, the        */
+                             /* communicator could not be created, or an all-reduce    */
+                             /* failed (sb_comm_*, sb_pcg_set_comm, solve/recon)       */
 } sb_status;
 
 /* Problem geometry.
@@ -90,11 +93,38 @@ typedef struct {
  *   sens    complex [B][C][d0][d1] coil sensitivities S_c
  *   mu, lambda, gamma  weights of Eq. original; gamma > 0 required
  *   cuda_stream  cudaStream_t to enqueue on (NULL = default stream)
+ *   comm    NULL (single GPU, or slice sharding: each rank its own context), or a coil-sharded
+ *           communicator (sb_comm_init_nccl; ndim = 3 only): `coils` and `sens` are then this
+ *           rank's coil shard and Lambda is built from the marginal over every rank's coils
+ *           (a collective call: every rank of comm must create its context)
  * Errors: SB_E_ARG, SB_E_DIM, SB_E_UNSUPPORTED_SIZE, SB_E_PARAM, SB_E_SINGULAR_K,
- *         SB_E_NOMEM, SB_E_CUDA.  Synchronises the stream before returning. */
+ *         SB_E_NOMEM, SB_E_CUDA, SB_E_COMM.  Synchronises the stream before returning. */
 sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const uint8_t* mask,
                         const sb_c64* sens, float mu, float lambda, float gamma,
-                        void* cuda_stream);
+                        void* cuda_stream, sb_comm* comm);
+
+/* Options (sb_set_option):
+ *   SB_OPT_PERSISTENT  1 (default) / 0: solve and reconstruct small batches of square line-mask
+ *                      problems (d0 = d1 in {64, 256}, Haar W, circulant M, single GPU, batch
+ *                      * d1 CTAs co-resident) with the persistent whole-GPU kernel (k_persist.cu;
+ *                      DESIGN.md "KR"); 0 forces the kernel sequence.  Results agree with the
+ *                      sequence to rounding (both are checked against the oracle). */
+#define SB_OPT_PERSISTENT 1
+/*   SB_OPT_PCG_CG      1 (default) / 0: inside the persistent kernel, run PCG with the
+ *                      Chronopoulos-Gear single-reduction recurrences (the iterates of
+ *                      PAPER.md:238 in exact arithmetic; s = A p carried by a recurrence, the
+ *                      two inner products of an iteration reduced together: two grid barriers
+ *                      per iteration instead of three) or with the standard recurrences. */
+#define SB_OPT_PCG_CG 2
+sb_status sb_set_option(sb_ctx* ctx, int32_t option, int32_t value);
+
+/* How the last sb_pcg_solve / sb_recon executed (for bench.py and tests). */
+#define SB_PATH_NONE 0
+#define SB_PATH_GRAPH 1          /* kernel sequence, device-driven loop in a CUDA graph       */
+#define SB_PATH_EAGER 2          /* kernel sequence, host-checked loop                        */
+#define SB_PATH_PERSISTENT 3     /* one cooperative launch of k_persist                       */
+#define SB_PATH_COIL_SHARDED 4   /* coil-sharded kernel sequence with NCCL all-reduces        */
+int32_t sb_last_path(const sb_ctx* ctx);
 
 /* Wavelet family of W in the SB shrink step: 0 = orthonormal Haar (default; reading A6),
  * 1 = periodized Daubechies-4, the paper's W (reading A32), same Mallat layout
@@ -150,12 +180,24 @@ sb_status sb_pcg_solve(sb_ctx* ctx, const sb_c64* b, sb_c64* x, const sb_pcg_opt
 typedef struct {
   int32_t n_outer, n_inner;  /* Algorithm 1 loops; n_inner must be 1 */
   sb_pcg_opts pcg;
+  int32_t stage_timers;      /* 1: fill the stage times of sb_recon_log on the kernel-   */
+                             /* sequence path (runs it eagerly: CUDA-event pairs around  */
+                             /* each stage).  The persistent path always fills them.     */
 } sb_recon_opts;
 
+/* Reconstruction log.  Stage times are device seconds summed over the call, split like the
+ * paper's cost discussion: step 4 (RHS), the PCG solves, steps 6-11
+ * (shrink/Bregman + regulariser RHS), steps 13-15 (data feedback).  Both paths form the RHS,
+ * the data feedback u += u1 - E^H E x and r0 = b - A x in ONE coil pass (the feedback reuses
+ * that pass's E^H E x), so its time is reported in rhs_s and feedback_s is 0.  init_s = step 1
+ * (u1 = sum_c S_c^H F^H y_c, RSS); build_s = the last Lambda build of this context (PAPER.md
+ * Table 2 analogue; create, sb_pcg_build_precond or sb_pcg_update_sens). */
 typedef struct {             /* host outputs (NULL members = not requested)               */
   int32_t* pcg_iters;        /* [n_outer * n_inner][B]                                    */
   float* final_relres;       /* [n_outer * n_inner][B]                                    */
   double total_ms;           /* device time of the whole call (CUDA events)               */
+  double rhs_s, pcg_s, shrink_s, feedback_s, build_s, init_s;
+  int32_t stages_valid;      /* 1 when the stage times were measured                      */
 } sb_recon_log;
 
 /* Split Bregman reconstruction, Algorithm 1 with per-problem PCG.
@@ -183,11 +225,12 @@ sb_status sb_sb_update3(sb_ctx* ctx, const sb_c64* x, sb_c64* bx, sb_c64* by, sb
 /* Real k (not 1/(N k)) as built, fp64 [B or 1][d0][d1] — parity output. */
 sb_status sb_pcg_get_k(sb_ctx* ctx, double* k_out);
 
-/* Kernel timing for bench.py's roofline: when enabled, CUDA events bracket every launch
- * of the matvec kernel (K1) on the context's stream and sb_get_kernel_time returns the
- * accumulated device ms, launch count, and the algorithmic bytes per launch. */
+/* Kernel timing for bench.py's roofline: when enabled, CUDA events bracket every launch of
+ * the matvec kernel (K1 / K1P; which = 0) and of the persistent kernel (KR; which = 2) on the
+ * context's stream (solves then run eagerly), and sb_get_kernel_time returns the accumulated
+ * device ms, the launch count and the algorithmic bytes per launch. */
 sb_status sb_set_kernel_timing(sb_ctx* ctx, int32_t enable);
-sb_status sb_get_kernel_time(sb_ctx* ctx, int32_t which /*0 = matvec K1, 1 = precond K2*/,
+sb_status sb_get_kernel_time(sb_ctx* ctx, int32_t which /*0 = matvec, 2 = persistent kernel*/,
                              double* ms, int64_t* launches, double* alg_bytes_per_launch);
 
 /* ------------------------------------------------------------------------------------
@@ -198,14 +241,14 @@ sb_status sb_get_kernel_time(sb_ctx* ctx, int32_t which /*0 = matvec K1, 1 = pre
  * that image forms the data term of A; the preconditioner, the regulariser,
  * the dots and the SB steps then run identically on every rank (the all-reduce result is
  * bitwise identical across ranks, so no scalar all-reduce is needed).  Lambda's coil
- * marginal, u_1 and the RSS init are all-reduced as well.  The PCG loop is host-driven in
- * this mode (no CUDA graph).  NCCL is loaded at run time (the process's libnccl.so.2, or
+ * marginal, u_1 and the RSS init are all-reduced as well.  NCCL is loaded at run time (the process's libnccl.so.2, or
  * SBPCG_NCCL_LIB).  For ndim = 3 contexts (2D batches shard by slice, with no collective).
  * ------------------------------------------------------------------------------------ */
-typedef struct sb_comm sb_comm;
 /* rank 0: a 128-byte NCCL unique id to broadcast to the other ranks (out of band). */
 sb_status sb_comm_unique_id(void* id_out);
-/* Collective over the `world` ranks; binds to the current CUDA device.  SB_E_COMM on failure. */
+/* Collective over the `world` ranks; binds to the current CUDA device.  SB_E_COMM on failure.
+ * sb_comm_init_nccl is the name SURVEY 8(b) uses; sb_comm_init is the same call. */
+sb_status sb_comm_init_nccl(const void* nccl_unique_id, int32_t rank, int32_t world, sb_comm** out);
 sb_status sb_comm_init(const void* id, int32_t rank, int32_t world, sb_comm** out);
 void sb_comm_destroy(sb_comm* comm);
 /* Attach (comm != NULL) or detach the communicator; rebuilds Lambda (collective). */

@@ -137,6 +137,48 @@ struct KcArgs {
 bool kc_supported(int M, int N);
 cudaError_t launch_kc(const KcArgs& a, const CUtensorMap* tmap16, cudaStream_t st);
 
+// Persistent whole-GPU reconstruction / solve for small batches of square line-mask problems
+// (k_persist.cu): one cooperative launch; CTA t of problem b owns image column
+// t (the matvec, the preconditioner's column transforms) and spectral row t (its row
+// transforms); the phases are separated by per-problem grid barriers.
+struct KrArgs {
+  int B, C, M, N, levels;
+  float mu, lam, gam;
+  const float2* sT;          // [B][C][N][M] coil maps, column-major per coil (transposed copy)
+  const float* rmask;        // [B or 1][M] = r/M
+  int rmask_bstride;
+  const float* lam_inv;      // [B][M][N] = 1/(N k)
+  const float2* tw;          // [M] forward twiddles
+  // image-layout vectors [B][M][N]
+  float2* x;                 // in: x0 (solve) / RSS init (recon); out: x
+  const float2* bvec;        // solve mode: b
+  float2* u;                 // recon: running u_j
+  const float2* u1;
+  float2* rhs;               // recon: rhs_reg (written by the SB phase)
+  SbArgs sb;                 // recon: SB state (bx/by double buffers, bw, rhs), parity 0 first
+  float2* bxs[2];
+  float2* bys[2];
+  // internal state
+  float2* Qs;                // [B][M][N] column spectrum of q (rows = spectral index)
+  float2* Sr;                // [B][M][N] column spectrum of r
+  float2* Tb;                // [B][N][M] row-phase output, column-major
+  double* part;              // [B][3][P] block partials
+  unsigned* bar;             // [B] barrier counters (zero at launch)
+  unsigned long long* stamp; // [32] stage cycle counters (nullable); [8, 20) loop segments
+  int prof;                  // 1: also time the PCG loop's segments (SBPCG_KR_PROF=1)
+  int cg;                    // 1: Chronopoulos-Gear recurrences (one reduction per iteration)
+  Loop L;
+  int n_outer;               // 0: one solve (b given) ; >= 1: SB reconstruction
+  float eps;
+  int maxit;
+};
+bool kr_supported(int M, int N, int levels);
+// CTAs one problem needs, and how many problems fit one cooperative launch on this device
+int kr_ctas(int M, int N);
+int kr_max_problems(int M, int N, int C);
+cudaError_t launch_kr(const KrArgs& a, cudaStream_t st);
+cudaError_t launch_transpose_sens(const float2* s, float2* sT, int BC, int M, int N, cudaStream_t st);
+
 // Plane kernels (k_plane*.cu): one G-CTA cluster per NY x NZ plane, DSMEM-exchanged 2D FFT.
 enum KPMode { KP_APPLY = 0, KP_PCG = 1, KP_RESID = 2, KP_PRECOND = 3, KP_ENCODE = 4, KP_ADJOINT = 5,
               KP_PRE2D = 6 };

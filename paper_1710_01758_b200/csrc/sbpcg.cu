@@ -141,10 +141,26 @@ struct sb_ctx {
   sb_status sticky = SB_OK;
   std::string err;
   int64_t launches = 0;
-  // kernel timing
+  // persistent reconstruction kernel (k_persist.cu): small batches of square line-mask problems
+  bool kr_ok = false;           // geometry and batch fit one cooperative launch (decided at create)
+  bool kr_on = true;            // sb_set_option(SB_OPT_PERSISTENT); env SBPCG_PERSIST=0 disables
+  bool kr_cg = true;            // sb_set_option(SB_OPT_PCG_CG): single-reduction recurrences in KR
+  float2* sT = nullptr;         // [B][C][N][M] column-major coil maps
+  unsigned* kbar = nullptr;     // [B] barrier counters
+  unsigned long long* kstamp = nullptr;  // [8] stage cycle counters
+  double kr_alg_bytes = 0;      // algorithmic bytes of the timed persistent launches
+  int last_path = 0;            // SB_PATH_* of the last solve / recon
+  // stage timers (sb_recon_log) and the Lambda build time
+  bool stage_timing = false;
+  double stage_s[5] = {0, 0, 0, 0, 0};  // rhs, pcg, shrink, feedback, init (seconds)
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> stage_ev;
+  std::vector<cudaEvent_t> stage_pool;
+  size_t stage_next = 0;
+  double build_s = 0;
+  // kernel timing (0 = matvec K1/K1P, 1 = unused, 2 = persistent kernel KR)
   bool timing = false;
-  double t_ms[2] = {0, 0};
-  int64_t t_n[2] = {0, 0};
+  double t_ms[3] = {0, 0, 0};
+  int64_t t_n[3] = {0, 0, 0};
   std::vector<cudaEvent_t> evpool;
   std::vector<std::pair<int, std::pair<int, int>>> evpend;  // (which, (ev0, ev1))
   size_t evnext = 0;
@@ -399,6 +415,47 @@ static void timing_collect(sb_ctx* c) {
   cudaGetLastError();
   c->evpend.clear();
   c->evnext = 0;
+}
+
+// Stage timers of sb_recon_log (SB_STAGE_*): an event pair around each stage on the context
+// stream (eager execution only); summed after the call's final synchronisation.
+enum { ST_RHS = 0, ST_PCG = 1, ST_SHRINK = 2, ST_FEEDBACK = 3, ST_INIT = 4 };
+static cudaEvent_t stage_event(sb_ctx* c) {
+  if (c->stage_next >= c->stage_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->stage_pool.push_back(e);
+  }
+  return c->stage_pool[c->stage_next++];
+}
+struct StageMark {  // records the start event; close() the end event
+  sb_ctx* c;
+  int stage;
+  cudaEvent_t e0 = nullptr;
+  cudaStream_t st;
+  StageMark(sb_ctx* cc, int sg, cudaStream_t s_) : c(cc), stage(sg), st(s_) {
+    if (c->stage_timing) {
+      e0 = stage_event(c);
+      cudaEventRecord(e0, st);
+    }
+  }
+  void close() {
+    if (e0) {
+      cudaEvent_t e1 = stage_event(c);
+      cudaEventRecord(e1, st);
+      c->stage_ev.push_back({stage, {e0, e1}});
+      e0 = nullptr;
+    }
+  }
+};
+static void stage_collect(sb_ctx* c) {
+  for (auto& se : c->stage_ev) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, se.second.first, se.second.second) == cudaSuccess) c->stage_s[se.first] += 1e-3 * ms;
+  }
+  cudaGetLastError();
+  c->stage_ev.clear();
+  c->stage_next = 0;
 }
 
 static sb_status allreduce(sb_ctx* c, void* buf, size_t count, int dtype, cudaStream_t st) {
@@ -756,15 +813,33 @@ static sb_status eager_solve(sb_ctx* c, int kind, const sb_pcg_opts* o, const fl
   g_use_pdl = env_flag("SBPCG_EAGER_PDL", true);
   sb_status s;
   cudaStream_t st = c->st;
-  if (kind == 0) s = seq_resid(c, L, c->bvec, false, false, false, o->eps, o->max_iters, st);
-  else if (kind == 1) {
+  // stage timers: the RESID kernel forms the RHS (step 4), the data feedback (steps 13-15) and
+  // r0 in one pass, so its time is reported as rhs_s (feedback_s stays 0: fused)
+  if (kind == 0) {
+    StageMark m(c, ST_RHS, st);
+    s = seq_resid(c, L, c->bvec, false, false, false, o->eps, o->max_iters, st);
+    m.close();
+  } else if (kind == 1) {
+    StageMark m0(c, ST_INIT, st);
     s = seq_init_recon(c, ydev, st);
+    m0.close();
+    StageMark m1(c, ST_RHS, st);
     if (!s) s = seq_resid(c, L, nullptr, true, false, false, o->eps, o->max_iters, st);
+    m1.close();
   } else {
+    StageMark m0(c, ST_SHRINK, st);
     s = seq_shrink(c, kind - 2, st);
+    m0.close();
+    StageMark m1(c, ST_RHS, st);
     if (!s) s = seq_resid(c, L, nullptr, true, true, true, o->eps, o->max_iters, st);
+    m1.close();
   }
   if (s) return s;
+  StageMark mp(c, ST_PCG, st);
+  struct Closer {
+    StageMark& m;
+    ~Closer() { m.close(); }
+  } closer{mp};
   if ((s = seq_precond(c, L, o->precond, 0, c->r, c->z, st))) return s;
   if (c->kc && o->precond == 1) {  // persistent cluster PCG
     if ((s = run_kc(c, L, st))) return s;
@@ -782,13 +857,99 @@ static sb_status eager_solve(sb_ctx* c, int kind, const sb_pcg_opts* o, const fl
 }
 
 static sb_status run_solve_kind(sb_ctx* c, int kind, const sb_pcg_opts* o, const float2* ydev) {
-  if (o->use_graph && !c->timing && !c->comm) {  // coil-sharded mode runs the host-driven loop
+  // coil-sharded mode runs the host-driven loop; stage timers need the eager sequence
+  if (o->use_graph && !c->timing && !c->comm && !c->stage_timing) {
     sb_status s = build_graph(c, kind, o, ydev);
     if (s) return s;
     CK(cudaGraphLaunch(c->gs[kind].exec, c->st));
+    c->last_path = SB_PATH_GRAPH;
     return SB_OK;
   }
+  c->last_path = c->comm ? SB_PATH_COIL_SHARDED : SB_PATH_EAGER;
   return eager_solve(c, kind, o, ydev);
+}
+
+// ------------------------------------------------------------------ persistent kernel (KR)
+static bool use_kr(sb_ctx* c, const sb_pcg_opts* o) {
+  return c->kr_ok && c->kr_on && o->precond == 1 && c->wavelet == 0 && !c->comm && !c->kc;
+}
+
+// One cooperative launch: n_outer = 0 solves A x = b (b in c->bvec, x0 in c->x); n_outer >= 1
+// runs the SB reconstruction after the init (u1, u, x = RSS already in place).
+static sb_status run_kr(sb_ctx* c, int n_outer, const sb_pcg_opts* o, int par0) {
+  KrArgs a;
+  memset(&a, 0, sizeof(a));
+  a.B = c->B;
+  a.C = c->C;
+  a.M = c->M;
+  a.N = c->N;
+  a.levels = c->L;
+  a.mu = c->mu;
+  a.lam = c->lam;
+  a.gam = c->gam;
+  a.sT = c->sT;
+  a.rmask = c->rowmask;
+  a.rmask_bstride = c->mask_shared ? 0 : c->M;
+  a.lam_inv = c->lam_inv;
+  a.tw = c->tw_m;
+  a.x = c->x;
+  a.bvec = c->bvec;
+  a.u = c->u;
+  a.u1 = c->u1;
+  a.rhs = c->rhs;
+  a.sb.B = c->B;
+  a.sb.M = c->M;
+  a.sb.N = c->N;
+  a.sb.levels = c->L;
+  a.sb.lam = c->lam;
+  a.sb.gam = c->gam;
+  a.sb.x = c->x;
+  a.sb.bw = c->bw;
+  a.sb.rhs = c->rhs;
+  for (int k = 0; k < 2; ++k) {
+    a.bxs[k] = c->bx[(k + par0) & 1];
+    a.bys[k] = c->by[(k + par0) & 1];
+  }
+  a.Qs = c->q;
+  a.Sr = c->r;
+  a.Tb = c->tmp;
+  a.part = c->P.p0;
+  a.bar = c->kbar;
+  a.stamp = c->kstamp;
+  a.prof = env_flag("SBPCG_KR_PROF", false) ? 1 : 0;
+  a.cg = c->kr_cg ? 1 : 0;
+  a.L = make_loop(c, 0ull);
+  a.n_outer = n_outer;
+  a.eps = o->eps;
+  a.maxit = o->max_iters;
+  CK(cudaMemsetAsync(c->kbar, 0, sizeof(unsigned) * c->B, c->st));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->timing) {
+    CK(launch_spin(c->st, 20000));
+    e0 = ev_get(c);
+    CK(cudaEventRecord(e0, c->st));
+  }
+  CK(launch_kr(a, c->st));
+  c->launches++;
+  if (c->timing) {
+    e1 = ev_get(c);
+    CK(cudaEventRecord(e1, c->st));
+    c->evpend.push_back({2, {(int)c->evnext - 2, (int)c->evnext - 1}});
+  }
+  c->last_path = SB_PATH_PERSISTENT;
+  return SB_OK;
+}
+
+// algorithmic bytes of one persistent launch: B_iter per PCG
+// iteration, plus the solve prelude and the SB step per problem and solve
+static double kr_bytes(sb_ctx* c, const std::vector<int32_t>& iters, int n_solves, bool sb) {
+  const double N = (double)c->img, C = (double)c->C, M = (double)c->M;
+  const double b_iter = 8.0 * N * (C + 10.0) + 4.0 * N + 4.0 * M;
+  const double b_pre = 8.0 * N * C + 84.0 * N + 4.0 * M;
+  const double b_sb = 64.0 * N;
+  double it = 0;
+  for (int32_t v : iters) it += v;
+  return it * b_iter + (double)n_solves * c->B * (b_pre + (sb ? b_sb : 0.0));
 }
 
 // ------------------------------------------------------------------ Lambda build
@@ -812,7 +973,23 @@ static cudaError_t lscratch(sb_ctx* c, int slot, T** p, size_t n) {
   return cudaSuccess;
 }
 
+static sb_status build_lambda_impl(sb_ctx* c);
+// Lambda build timed with an event pair (sb_recon_log.build_s; Table 2 analogue).
 static sb_status build_lambda(sb_ctx* c) {
+  cudaEvent_t e0 = stage_event(c), e1 = stage_event(c);
+  c->stage_next -= 2;  // scratch use: not part of a recon's stage list
+  CK(cudaEventRecord(e0, c->st));
+  sb_status s = build_lambda_impl(c);
+  if (s) return s;
+  CK(cudaEventRecord(e1, c->st));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  c->build_s = 1e-3 * ms;
+  return SB_OK;
+}
+
+static sb_status build_lambda_impl(sb_ctx* c) {
   if (c->ndim == 3) return build_lambda3(c);
   LamArgs a;
   memset(&a, 0, sizeof(a));
@@ -1001,12 +1178,13 @@ void sb_pcg_destroy(sb_ctx* c) {
     if (g.graph) cudaGraphDestroy(g.graph);
   }
   for (auto e : c->evpool) cudaEventDestroy(e);
+  for (auto e : c->stage_pool) cudaEventDestroy(e);
   void* bufs[] = {c->sens, c->mask, c->rowmask, c->lam_inv, c->kbuf, c->tw_m, c->tw_n, c->twd_m, c->twd_n,
                   c->x, c->r, c->z, c->q, c->p0, c->p1, c->tmp, c->bvec, c->u, c->u1, c->rhs,
                   c->bx[0], c->bx[1], c->by[0], c->by[1], c->bw, c->tmpc, c->stage_in, c->stage_out,
                   c->scal, c->ctl, c->counters, c->P.p0, c->P.p1, c->P.cnt, c->hist, c->log_iters, c->log_relres,
                   c->pmask, c->tw_y, c->tw_z, c->twd_y, c->twd_z, c->bz[0], c->bz[1], c->accbuf, c->jinv,
-                  c->wbuf};
+                  c->wbuf, c->sT, c->kbar, c->kstamp};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (void* p : c->lscr)
@@ -1017,7 +1195,7 @@ void sb_pcg_destroy(sb_ctx* c) {
 }
 
 sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const uint8_t* mask, const sb_c64* sens,
-                        float mu, float lambda, float gamma, void* cuda_stream) {
+                        float mu, float lambda, float gamma, void* cuda_stream, sb_comm* comm) {
   if (!out) return SB_E_ARG;
   *out = nullptr;
   if (!dims || !mask || !sens) return SB_E_ARG;
@@ -1043,6 +1221,7 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   if (!(gamma > 0.f) || mu < 0.f || lambda < 0.f || !std::isfinite(mu) || !std::isfinite(lambda) ||
       !std::isfinite(gamma))
     return SB_E_PARAM;
+  if (comm && !d3) return SB_E_UNSUPPORTED_SIZE;  // coil sharding is the 3D mode (2D batches shard by slice)
 
   sb_ctx* c = new sb_ctx();
   c->st = (cudaStream_t)cuda_stream;
@@ -1148,7 +1327,9 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
     const bool small = (int64_t)c->B * gpre <= 2 * 148;
     const char* pe = getenv("SBPCG_PRE2D");
     c->pre2d = kp2_supported((int)M, (int)N) && (pe ? pe[0] == '1' : small);
-    if (sep && cudaMemcpy(c->rowmask, rm.data(), rm.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
+    if (sep && (cudaMemcpyAsync(c->rowmask, rm.data(), rm.size() * sizeof(float), cudaMemcpyHostToDevice, c->st) !=
+                    cudaSuccess ||
+                cudaStreamSynchronize(c->st) != cudaSuccess))
       return bail(SB_E_CUDA);
   } else {
     // 3D: the mask must be constant along the readout d0 (BASELINE config 5):
@@ -1162,29 +1343,36 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
           return SB_E_UNSUPPORTED_SIZE;
         }
     for (int b = 0; b < nm; ++b)
-      if (cudaMemcpy(c->pmask + (size_t)b * pn, hm.data() + (size_t)b * img, pn, cudaMemcpyHostToDevice) !=
+      if (cudaMemcpyAsync(c->pmask + (size_t)b * pn, hm.data() + (size_t)b * img, pn, cudaMemcpyHostToDevice, c->st) !=
           cudaSuccess)
         return bail(SB_E_CUDA);
+    if (cudaStreamSynchronize(c->st) != cudaSuccess) return bail(SB_E_CUDA);
     c->separable = false;
     c->plane = true;
   }
   // twiddles
   auto tm = make_tw<float2>((int)M), tn = make_tw<float2>((int)N);
   auto tdm = make_tw<double2>((int)M), tdn = make_tw<double2>((int)N);
-  if (cudaMemcpy(c->tw_m, tm.data(), M * sizeof(float2), cudaMemcpyHostToDevice) ||
-      cudaMemcpy(c->tw_n, tn.data(), N * sizeof(float2), cudaMemcpyHostToDevice) ||
-      cudaMemcpy(c->twd_m, tdm.data(), M * sizeof(double2), cudaMemcpyHostToDevice) ||
-      cudaMemcpy(c->twd_n, tdn.data(), N * sizeof(double2), cudaMemcpyHostToDevice))
+  // twiddle uploads on the context stream; the host tables live until the synchronisation below
+  if (cudaMemcpyAsync(c->tw_m, tm.data(), M * sizeof(float2), cudaMemcpyHostToDevice, c->st) ||
+      cudaMemcpyAsync(c->tw_n, tn.data(), N * sizeof(float2), cudaMemcpyHostToDevice, c->st) ||
+      cudaMemcpyAsync(c->twd_m, tdm.data(), M * sizeof(double2), cudaMemcpyHostToDevice, c->st) ||
+      cudaMemcpyAsync(c->twd_n, tdn.data(), N * sizeof(double2), cudaMemcpyHostToDevice, c->st))
     return bail(SB_E_CUDA);
+  std::vector<float2> ty, tz;
+  std::vector<double2> tdy, tdz;
   if (d3) {
-    auto ty = make_tw<float2>((int)D1), tz = make_tw<float2>((int)D2);
-    auto tdy = make_tw<double2>((int)D1), tdz = make_tw<double2>((int)D2);
-    if (cudaMemcpy(c->tw_y, ty.data(), D1 * sizeof(float2), cudaMemcpyHostToDevice) ||
-        cudaMemcpy(c->tw_z, tz.data(), D2 * sizeof(float2), cudaMemcpyHostToDevice) ||
-        cudaMemcpy(c->twd_y, tdy.data(), D1 * sizeof(double2), cudaMemcpyHostToDevice) ||
-        cudaMemcpy(c->twd_z, tdz.data(), D2 * sizeof(double2), cudaMemcpyHostToDevice))
+    ty = make_tw<float2>((int)D1);
+    tz = make_tw<float2>((int)D2);
+    tdy = make_tw<double2>((int)D1);
+    tdz = make_tw<double2>((int)D2);
+    if (cudaMemcpyAsync(c->tw_y, ty.data(), D1 * sizeof(float2), cudaMemcpyHostToDevice, c->st) ||
+        cudaMemcpyAsync(c->tw_z, tz.data(), D2 * sizeof(float2), cudaMemcpyHostToDevice, c->st) ||
+        cudaMemcpyAsync(c->twd_y, tdy.data(), D1 * sizeof(double2), cudaMemcpyHostToDevice, c->st) ||
+        cudaMemcpyAsync(c->twd_z, tdz.data(), D2 * sizeof(double2), cudaMemcpyHostToDevice, c->st))
       return bail(SB_E_CUDA);
   }
+  if (cudaStreamSynchronize(c->st) != cudaSuccess) return bail(SB_E_CUDA);
   // zero state
   for (auto v : vecs)
     if (cudaMemsetAsync(*v, 0, BN * sizeof(float2), c->st) != cudaSuccess) return bail(SB_E_CUDA);
@@ -1226,6 +1414,30 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
     sb_pcg_destroy(c);
     return s;
   }
+  // the persistent whole-GPU kernel (k_persist.cu) for small batches of square line-mask
+  // problems: a column-major copy of the coil maps, barrier counters, stage counters
+  c->kr_on = env_flag("SBPCG_PERSIST", true);
+  c->kr_cg = env_flag("SBPCG_CG", true);
+  c->kr_ok = !d3 && c->separable && kr_supported(c->M, c->N, c->L) && c->B <= kr_max_problems(c->M, c->N, c->C);
+  if (!s && c->kr_ok) {
+    if (dalloc(&c->sT, BCN) != cudaSuccess || dalloc(&c->kbar, c->B) != cudaSuccess ||
+        dalloc(&c->kstamp, 32) != cudaSuccess) {
+      cudaGetLastError();
+      sb_pcg_destroy(c);
+      return SB_E_NOMEM;
+    }
+    if (launch_transpose_sens(c->sens, c->sT, c->B * c->C, c->M, c->N, c->st) != cudaSuccess) {
+      sb_pcg_destroy(c);
+      return SB_E_CUDA;
+    }
+  }
+  if (!s && comm) {  // coil-sharded context (collective: Lambda from every rank's coils)
+    if (dalloc(&c->accbuf, (size_t)c->B * c->img) != cudaSuccess) {
+      sb_pcg_destroy(c);
+      return SB_E_NOMEM;
+    }
+    c->comm = comm;
+  }
   s = build_lambda(c);
   if (s) {
     sb_pcg_destroy(c);
@@ -1234,6 +1446,24 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   *out = c;
   return SB_OK;
 }
+
+sb_status sb_set_option(sb_ctx* c, int32_t option, int32_t value) {
+  sb_status s = check_ready(c);
+  if (s) return s;
+  switch (option) {
+    case SB_OPT_PERSISTENT:
+      if (value != 0 && value != 1) return fail(c, SB_E_ARG, "SB_OPT_PERSISTENT takes 0 or 1");
+      c->kr_on = value != 0;
+      return SB_OK;
+    case SB_OPT_PCG_CG:
+      if (value != 0 && value != 1) return fail(c, SB_E_ARG, "SB_OPT_PCG_CG takes 0 or 1");
+      c->kr_cg = value != 0;
+      return SB_OK;
+    default: return fail(c, SB_E_ARG, "unknown option");
+  }
+}
+
+int32_t sb_last_path(const sb_ctx* c) { return c ? c->last_path : SB_PATH_NONE; }
 
 sb_status sb_comm_unique_id(void* id_out) {
   if (!id_out) return SB_E_ARG;
@@ -1259,6 +1489,10 @@ sb_status sb_comm_init(const void* id, int32_t rank, int32_t world, sb_comm** ou
   cm->world = world;
   *out = cm;
   return SB_OK;
+}
+
+sb_status sb_comm_init_nccl(const void* nccl_unique_id, int32_t rank, int32_t world, sb_comm** out) {
+  return sb_comm_init(nccl_unique_id, rank, world, out);
 }
 
 void sb_comm_destroy(sb_comm* cm) {
@@ -1373,6 +1607,7 @@ sb_status sb_pcg_update_sens(sb_ctx* c, const sb_c64* sens) {
   const size_t bytes = (size_t)c->B * c->C * c->img * sizeof(float2);
   CK(cudaMemcpyAsync(c->sens, sens, bytes, is_device_ptr(sens) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                      c->st));
+  if (c->sT) CK(launch_transpose_sens(c->sens, c->sT, c->B * c->C, c->M, c->N, c->st));
   if (c->jinv) {  // Jacobi diagonal depends on the maps: rebuilt on next use
     cudaFree(c->jinv);
     c->jinv = nullptr;
@@ -1540,13 +1775,21 @@ sb_status sb_pcg_solve(sb_ctx* c, const sb_c64* b, sb_c64* x, const sb_pcg_opts*
   CK(cudaMemcpyAsync(c->x, x, bytes, xdev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
   CK(cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st));
   if (c->timing) c->evnext = 0;
-  if ((s = run_solve_kind(c, 0, o, nullptr))) return s;
+  const bool kr = use_kr(c, o);
+  if ((s = kr ? run_kr(c, 0, o, 0) : run_solve_kind(c, 0, o, nullptr))) return s;
   CK(cudaMemcpyAsync(x, c->x, bytes, xdev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
-  if (c->timing) timing_collect(c);
   std::vector<Scal> hs(c->B);
   CK(cudaMemcpy(hs.data(), c->scal, sizeof(Scal) * c->B, cudaMemcpyDeviceToHost));
-  if (o->use_graph && !c->timing) {
+  if (c->timing) {
+    if (kr) {
+      std::vector<int32_t> it(c->B);
+      for (int i = 0; i < c->B; ++i) it[i] = hs[i].iter;
+      c->kr_alg_bytes += kr_bytes(c, it, 1, false);
+    }
+    timing_collect(c);
+  }
+  if (o->use_graph && !c->timing && !kr) {
     int mx = 0;
     for (auto& h : hs) mx = std::max(mx, h.iter);
     const GraphSlot& g0 = c->gs[0];
@@ -1594,14 +1837,33 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
   CK(cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st));
   if (c->timing) c->evnext = 0;
   const sb_pcg_opts* o = &ro->pcg;
-  if ((s = run_solve_kind(c, 1, o, (const float2*)yd))) return s;
-  for (int j = 1; j < ro->n_outer; ++j) {
-    const int par = (j - 1) & 1;  // b_x/b_y buffer parity
-    if ((s = run_solve_kind(c, 2 + par, o, nullptr))) return s;
+  const bool kr = use_kr(c, o);
+  c->stage_timing = kr ? false : (ro->stage_timers != 0);
+  for (double& v : c->stage_s) v = 0.0;
+  c->stage_ev.clear();
+  c->stage_next = 0;
+  if (kr) {
+    // Alg. 1 step 1 (u1, x = RSS) by the column/row passes, then the whole SB loop in one
+    // cooperative launch (including the final shrink/Bregman step)
+    cudaEvent_t ei0 = stage_event(c), ei1 = stage_event(c);
+    CK(cudaEventRecord(ei0, c->st));
+    if ((s = seq_init_recon(c, (const float2*)yd, c->st))) return s;
+    CK(cudaEventRecord(ei1, c->st));
+    c->stage_ev.push_back({ST_INIT, {ei0, ei1}});
+    CK(cudaMemsetAsync(c->kstamp, 0, 32 * sizeof(unsigned long long), c->st));
+    if ((s = run_kr(c, ro->n_outer, o, 0))) return s;
+  } else {
+    if ((s = run_solve_kind(c, 1, o, (const float2*)yd))) return s;
+    for (int j = 1; j < ro->n_outer; ++j) {
+      const int par = (j - 1) & 1;  // b_x/b_y buffer parity
+      if ((s = run_solve_kind(c, 2 + par, o, nullptr))) return s;
+    }
+    // final shrink/Bregman step of the last inner iteration (Alg. 1 steps 6-11); the final
+    // data feedback (steps 13-15) does not change x and is skipped.
+    StageMark m(c, ST_SHRINK, c->st);
+    if ((s = seq_shrink(c, (ro->n_outer - 1) & 1, c->st))) return s;
+    m.close();
   }
-  // final shrink/Bregman step of the last inner iteration (Alg. 1 steps 6-11); the final
-  // data feedback (steps 13-15) does not change x and is skipped.
-  if ((s = seq_shrink(c, (ro->n_outer - 1) & 1, c->st))) return s;
   CK(cudaMemcpyAsync(x_out, c->x, bytes, is_device_ptr(x_out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                      c->st));
   CK(cudaEventRecord(e1, c->st));
@@ -1610,12 +1872,31 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  if (c->timing) timing_collect(c);
+  const bool stages = kr || c->stage_timing;
+  stage_collect(c);
+  if (kr) {  // the kernel's stage cycle counters, converted with its own cycles -> ns ratio
+    unsigned long long hst[32];
+    CK(cudaMemcpy(hst, c->kstamp, sizeof(hst), cudaMemcpyDeviceToHost));
+    if (env_flag("SBPCG_KR_PROF", false)) {  // loop segment profile (stderr)
+      fprintf(stderr, "KR segments (ns, all iterations):");
+      for (int k = 0; k < 10; ++k) fprintf(stderr, " s%d=%.0f", k, hst[3] ? (double)hst[8 + k] * hst[4] / hst[3] : 0.0);
+      fprintf(stderr, "\n");
+    }
+    const double s_per_cyc = hst[3] > 0 ? 1e-9 * (double)hst[4] / (double)hst[3] : 0.0;
+    c->stage_s[ST_RHS] += s_per_cyc * (double)hst[0];
+    c->stage_s[ST_PCG] += s_per_cyc * (double)hst[1];
+    c->stage_s[ST_SHRINK] += s_per_cyc * (double)hst[2];
+  }
+  c->stage_timing = false;
   std::vector<int32_t> li((size_t)ro->n_outer * c->B);
   std::vector<float> lr((size_t)ro->n_outer * c->B);
   CK(cudaMemcpy(li.data(), c->log_iters, li.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(lr.data(), c->log_relres, lr.size() * sizeof(float), cudaMemcpyDeviceToHost));
-  if (o->use_graph && !c->timing) {
+  if (c->timing) {
+    if (kr) c->kr_alg_bytes += kr_bytes(c, li, ro->n_outer, true);
+    timing_collect(c);
+  }
+  if (o->use_graph && !c->timing && !kr) {
     for (int j = 0; j < ro->n_outer; ++j) {
       int mx = 0;
       for (int b = 0; b < c->B; ++b) mx = std::max(mx, li[(size_t)j * c->B + b]);
@@ -1627,6 +1908,13 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
     if (log->pcg_iters) memcpy(log->pcg_iters, li.data(), li.size() * sizeof(int32_t));
     if (log->final_relres) memcpy(log->final_relres, lr.data(), lr.size() * sizeof(float));
     log->total_ms = ms;
+    log->rhs_s = c->stage_s[ST_RHS];
+    log->pcg_s = c->stage_s[ST_PCG];
+    log->shrink_s = c->stage_s[ST_SHRINK];
+    log->feedback_s = c->stage_s[ST_FEEDBACK];
+    log->init_s = c->stage_s[ST_INIT];
+    log->build_s = c->build_s;
+    log->stages_valid = stages ? 1 : 0;
   }
   return status_from_scal(c);
 }
@@ -1689,17 +1977,24 @@ sb_status sb_pcg_get_k(sb_ctx* c, double* k_out) {
 sb_status sb_set_kernel_timing(sb_ctx* c, int32_t enable) {
   if (!c) return SB_E_ARG;
   c->timing = enable != 0;
-  c->t_ms[0] = c->t_ms[1] = 0;
-  c->t_n[0] = c->t_n[1] = 0;
+  for (int k = 0; k < 3; ++k) {
+    c->t_ms[k] = 0;
+    c->t_n[k] = 0;
+  }
+  c->kr_alg_bytes = 0;
   cudaStreamSynchronize(c->st);
   if (cudaMemset(c->counters, 0, sizeof(Counters)) != cudaSuccess) return fail(c, SB_E_CUDA, "memset counters");
   return SB_OK;
 }
 
 sb_status sb_get_kernel_time(sb_ctx* c, int32_t which, double* ms, int64_t* launches, double* alg_bytes) {
-  if (!c || which < 0 || which > 1) return SB_E_ARG;
+  if (!c || which < 0 || which > 2) return SB_E_ARG;
   if (ms) *ms = c->t_ms[which];
   if (launches) *launches = c->t_n[which];
+  if (alg_bytes && which == 2) {
+    *alg_bytes = c->t_n[2] > 0 ? c->kr_alg_bytes / (double)c->t_n[2] : 0.0;
+    return SB_OK;
+  }
   if (alg_bytes) {
     // K1 algorithmic bytes per problem-launch: coil maps 8NC
     // + z, p_{k-1} (and halo), x read + x, p_k, q written (6 x 8N) + row mask (4M);

@@ -37,18 +37,28 @@ class SbPcgStats(C.Structure):
 
 
 class SbReconOpts(C.Structure):
-    _fields_ = [("n_outer", C.c_int32), ("n_inner", C.c_int32), ("pcg", SbPcgOpts)]
+    _fields_ = [("n_outer", C.c_int32), ("n_inner", C.c_int32), ("pcg", SbPcgOpts),
+                ("stage_timers", C.c_int32)]
 
 
 class SbReconLog(C.Structure):
     _fields_ = [("pcg_iters", C.POINTER(C.c_int32)), ("final_relres", C.POINTER(C.c_float)),
-                ("total_ms", C.c_double)]
+                ("total_ms", C.c_double), ("rhs_s", C.c_double), ("pcg_s", C.c_double),
+                ("shrink_s", C.c_double), ("feedback_s", C.c_double), ("build_s", C.c_double),
+                ("init_s", C.c_double), ("stages_valid", C.c_int32)]
+
+
+SB_OPT_PERSISTENT = 1
+SB_OPT_PCG_CG = 2
+PATHS = {0: "none", 1: "graph", 2: "eager", 3: "persistent", 4: "coil-sharded"}
 
 
 _vp = C.c_void_p
 _sig = {
     "sb_pcg_create": (C.c_int, [C.POINTER(_vp), C.POINTER(SbDims), C.c_int32, _vp, _vp, C.c_float,
-                                C.c_float, C.c_float, _vp]),
+                                C.c_float, C.c_float, _vp, _vp]),
+    "sb_set_option": (C.c_int, [_vp, C.c_int32, C.c_int32]),
+    "sb_last_path": (C.c_int32, [_vp]),
     "sb_pcg_build_precond": (C.c_int, [_vp]),
     "sb_set_wavelet": (C.c_int, [_vp, C.c_int32]),
     "sb_pcg_update_sens": (C.c_int, [_vp, _vp]),
@@ -67,6 +77,7 @@ _sig = {
     "sb_kernel_launch_count": (C.c_int64, [_vp]),
     "sb_comm_unique_id": (C.c_int, [_vp]),
     "sb_comm_init": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(_vp)]),
+    "sb_comm_init_nccl": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(_vp)]),
     "sb_comm_destroy": (None, [_vp]),
     "sb_pcg_set_comm": (C.c_int, [_vp, _vp]),
     "sb_normalize_sens": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_int64, C.c_int32, _vp, _vp]),
@@ -107,10 +118,13 @@ class SbPcg:
     circulant preconditioner M^{-1} = F^H diag{k}^{-1} F."""
 
     def __init__(self, sens: torch.Tensor, mask: torch.Tensor, mu: float, lam: float, gamma: float,
-                 levels: int = 1, stream: Optional[torch.cuda.Stream] = None, wavelet: str = "haar"):
+                 levels: int = 1, stream: Optional[torch.cuda.Stream] = None, wavelet: str = "haar",
+                 comm: Optional["SbComm"] = None, persistent: bool = True):
         """sens: complex64 [B,C,M,N] (2D) or [B,C,D0,D1,D2] (3D; a 4D tensor is read as 2D);
         mask: uint8 [B,*image] or [*image] (shared).  3D masks must be constant along D0.
-        wavelet: "haar" (reading A6) or "d4" (the paper's Daubechies-4)."""
+        wavelet: "haar" (reading A6) or "d4" (the paper's Daubechies-4).
+        comm: coil-sharded communicator (3D; sens is then this rank's coil shard).
+        persistent: allow the persistent whole-GPU kernel (SB_OPT_PERSISTENT)."""
         if sens.dtype != torch.complex64 or mask.dtype != torch.uint8:
             raise TypeError("sens must be complex64 [B,C,*image], mask uint8 [B,*image] or [*image]")
         if sens.dim() == 3:
@@ -131,11 +145,17 @@ class SbPcg:
         shp = list(self.image) + [0] * (3 - nd)
         d = SbDims(nd, (C.c_int64 * 3)(*shp), B, levels, 1 if shared else 0)
         h = _vp()
+        if self._mask.numel() not in (int(np.prod(self.image)), B * int(np.prod(self.image))):
+            raise ValueError("mask must be [B,*image] or [*image]")
+        self._comm = comm
         st = _lib.sb_pcg_create(C.byref(h), C.byref(d), Cc, _ptr(self._mask), _ptr(self._sens),
-                                float(mu), float(lam), float(gamma), _vp(self._stream.cuda_stream))
+                                float(mu), float(lam), float(gamma), _vp(self._stream.cuda_stream),
+                                comm._h if comm is not None else None)
         if st != 0:
             raise SbError(st, "sb_pcg_create failed")
         self._h = h
+        if not persistent:
+            self._check(_lib.sb_set_option(self._h, SB_OPT_PERSISTENT, 0), "set_option")
         self.mu, self.lam, self.gamma, self.levels = mu, lam, gamma, levels
         if wavelet not in ("haar", "d4"):
             raise ValueError("wavelet must be 'haar' or 'd4'")
@@ -159,6 +179,22 @@ class SbPcg:
         except Exception:
             pass
 
+    def _arg(self, t: torch.Tensor, name: str, coils: bool = False) -> int:
+        """Pointer of an image ([B,*image]) or coil-stack ([B,C,*image]) argument after checking
+        dtype, shape and device (the library copies B*C*img complex values from/to it)."""
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{name}: expected a torch tensor")
+        shape = ((self.B, self.C) if coils else (self.B,)) + self.image
+        if t.dtype != torch.complex64:
+            raise TypeError(f"{name}: dtype must be complex64, got {t.dtype}")
+        if tuple(t.shape) != shape:
+            raise ValueError(f"{name}: shape must be {shape}, got {tuple(t.shape)}")
+        if t.device.type == "cuda" and t.device != self.device:
+            raise ValueError(f"{name}: on {t.device}, the context is on {self.device}")
+        if t.device.type not in ("cuda", "cpu"):
+            raise ValueError(f"{name}: device must be the context's CUDA device or the CPU")
+        return _ptr(t)
+
     def _img(self, like: Optional[torch.Tensor] = None, coils: bool = False, device=None):
         shape = (self.B, self.C) + self.image if coils else (self.B,) + self.image
         dev = device if device is not None else (like.device if like is not None else self.device)
@@ -180,22 +216,23 @@ class SbPcg:
 
     def apply_A(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         y = out if out is not None else self._img(x)
-        self._check(_lib.sb_pcg_apply_A(self._h, _ptr(x), _ptr(y)), "apply_A")
+        self._check(_lib.sb_pcg_apply_A(self._h, self._arg(x, "x"), self._arg(y, "out")), "apply_A")
         return y
 
     def apply_Pinv(self, r: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         z = out if out is not None else self._img(r)
-        self._check(_lib.sb_pcg_apply_Pinv(self._h, _ptr(r), _ptr(z)), "apply_Pinv")
+        self._check(_lib.sb_pcg_apply_Pinv(self._h, self._arg(r, "r"), self._arg(z, "out")), "apply_Pinv")
         return z
 
     def encode(self, x: torch.Tensor, full: bool = False, out: Optional[torch.Tensor] = None):
         y = out if out is not None else self._img(x, coils=True)
-        self._check(_lib.sb_encode(self._h, _ptr(x), _ptr(y), 1 if full else 0), "encode")
+        self._check(_lib.sb_encode(self._h, self._arg(x, "x"), self._arg(y, "out", coils=True), 1 if full else 0),
+                    "encode")
         return y
 
     def adjoint(self, y: torch.Tensor, out: Optional[torch.Tensor] = None):
         x = out if out is not None else self._img(y)
-        self._check(_lib.sb_adjoint(self._h, _ptr(y), _ptr(x)), "adjoint")
+        self._check(_lib.sb_adjoint(self._h, self._arg(y, "y", coils=True), self._arg(x, "out")), "adjoint")
         return x
 
     def get_k(self) -> torch.Tensor:
@@ -212,7 +249,8 @@ class SbPcg:
         hist = (C.c_float * (self.B * (max_iters + 1)))() if history else None
         st = SbPcgStats(iters, rel, conv, hist)
         o = SbPcgOpts(float(eps), int(max_iters), int(precond), 1 if use_graph else 0)
-        self._check(_lib.sb_pcg_solve(self._h, _ptr(b), _ptr(x), C.byref(o), C.byref(st)), "solve")
+        self._check(_lib.sb_pcg_solve(self._h, self._arg(b, "b"), self._arg(x, "x0"), C.byref(o), C.byref(st)),
+                    "solve")
         out = dict(iters=list(iters), final_relres=list(rel), converged=[bool(v) for v in conv])
         if history:
             out["relres_hist"] = [list(hist[i * (max_iters + 1):(i + 1) * (max_iters + 1)])
@@ -220,20 +258,40 @@ class SbPcg:
         return x, out
 
     def recon(self, y: torch.Tensor, n_outer: int, eps: float = 1e-4, max_iters: int = 50,
-              precond: int = 1, use_graph: bool = True, out: Optional[torch.Tensor] = None):
+              precond: int = 1, use_graph: bool = True, out: Optional[torch.Tensor] = None,
+              stage_timers: bool = False):
         x = out if out is not None else self._img(y)
         it = (C.c_int32 * (n_outer * self.B))()
         rel = (C.c_float * (n_outer * self.B))()
-        log = SbReconLog(it, rel, 0.0)
+        log = SbReconLog(it, rel)
         o = SbReconOpts(int(n_outer), 1, SbPcgOpts(float(eps), int(max_iters), int(precond),
-                                                   1 if use_graph else 0))
-        self._check(_lib.sb_recon(self._h, _ptr(y), C.byref(o), _ptr(x), C.byref(log)), "recon")
+                                                   1 if use_graph else 0), 1 if stage_timers else 0)
+        self._check(_lib.sb_recon(self._h, self._arg(y, "y", coils=True), C.byref(o), self._arg(x, "out"),
+                                  C.byref(log)), "recon")
         iters = [[it[j * self.B + b] for b in range(self.B)] for j in range(n_outer)]
         rels = [[rel[j * self.B + b] for b in range(self.B)] for j in range(n_outer)]
-        return x, dict(pcg_iters=iters, final_relres=rels, total_ms=log.total_ms)
+        stages = None
+        if log.stages_valid:
+            stages = dict(rhs_s=log.rhs_s, pcg_s=log.pcg_s, shrink_s=log.shrink_s,
+                          feedback_s=log.feedback_s, init_s=log.init_s)
+        return x, dict(pcg_iters=iters, final_relres=rels, total_ms=log.total_ms, stages=stages,
+                       build_s=log.build_s, path=self.last_path())
+
+    def last_path(self) -> str:
+        """How the last solve / recon ran: graph, eager, persistent or coil-sharded."""
+        return PATHS.get(int(_lib.sb_last_path(self._h)), "?")
+
+    def set_persistent(self, on: bool):
+        self._check(_lib.sb_set_option(self._h, SB_OPT_PERSISTENT, 1 if on else 0), "set_option")
+
+    def set_pcg_cg(self, on: bool):
+        """Persistent kernel: Chronopoulos-Gear single-reduction PCG (default) or standard."""
+        self._check(_lib.sb_set_option(self._h, SB_OPT_PCG_CG, 1 if on else 0), "set_option")
 
     def sb_update(self, x, bx, by, bw, bz=None):
         """One shrink/Bregman step; 3D contexts also take and return b_z (returned last)."""
+        for t, nm in ((x, "x"), (bx, "bx"), (by, "by"), (bw, "bw")) + (((bz, "bz"),) if self.ndim == 3 else ()):
+            self._arg(t, nm)
         bx, by, bw = bx.clone(), by.clone(), bw.clone()
         rhs = torch.empty_like(x)
         if self.ndim == 3:
@@ -275,7 +333,7 @@ class SbComm:
             raise ValueError("NCCL unique id must be 128 bytes")
         buf = C.create_string_buffer(uid, 128)
         h = _vp()
-        st = _lib.sb_comm_init(buf, int(rank), int(world), C.byref(h))
+        st = _lib.sb_comm_init_nccl(buf, int(rank), int(world), C.byref(h))
         if st != 0:
             raise SbError(st, "sb_comm_init failed")
         self._h, self.rank, self.world = h, rank, world

@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol(lib):
     for s in _declared():
         assert getattr(h, s) is not None
     h.sb_abi_version.restype = ctypes.c_int32
-    assert h.sb_abi_version() == 1
+    assert h.sb_abi_version() == 2
     h.sb_status_str.restype = ctypes.c_char_p
     assert h.sb_status_str(7) == b"SB_E_INDEFINITE"
 
@@ -55,7 +55,7 @@ def test_library_is_sm100a_with_tma(lib):
 
 def test_binding_module_imports_without_gpu(lib):
     import paper_1710_01758_b200 as p
-    assert p.abi_version() == 1
+    assert p.abi_version() == 2
 
 
 def test_no_oracle_on_product_path():
