@@ -68,8 +68,8 @@ struct KrSmem {
   float2 tw[M];
   float li[M];                        // Lambda^{-1} of spectral row t
   float rm[M];                        // r/M (row mask)
-  double red[32];
-  double bc[4];                       // broadcast of reduced scalars
+  double red[48];
+  double bc[8];                       // broadcast of reduced scalars
   long long tclk, tclk0;              // stage timer state (one thread of one CTA)
   unsigned long long tgt0, tstage[3];
   // followed (SMC) by the coil-map column lines [C][M]
@@ -164,7 +164,7 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
   }
 }
 
-// Block reduction of NS partials in two halves so other work can sit between them:
+// Block reduction of NS partials (NS <= 6) in two halves so other work can sit between them:
 // red_warps() leaves one fixed-tree warp sum per (slot, warp) in red[s * 8 + warp] and ends with
 // __syncthreads; red_final() (lanes of one warp) adds the warp sums in warp order (lane 0 result).
 template <int NS>
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
   float2 twr[N1];
   load_twr<M>(twr, S.tw, j);
 
-  double* part = a.part + (size_t)b * 3 * P;
+  double* part = a.part + (size_t)b * 8 * P;  // 6 slots used (Chronopoulos-Gear phase C)
   float2* xl = S.u.xch + line * XL;
 
   // A-product epilogue for row i: reg = lambda L v + gamma v from S.pc
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
         seg(0);
         kr_dataterm<M, SMC>(S, S.zc[1], coils, sTb, C, xl, twr);
         seg(1);
-        double dd = 0.0, drr = 0.0;
+        double dd = 0.0, drr = 0.0, de = 0.0, dq = 0.0, dp = 0.0;
         for (int i = tid; i < M; i += NT) {
           const float2 av = S.qs[i];
           float2 z;
@@ -551,26 +551,31 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
           dd += (double)w.x * z.x + (double)w.y * z.y;
           const float2 r = S.rs[i];
           drr += (double)r.x * r.x + (double)r.y * r.y;
+          if (kc > 0) {  // Re<z, s_kc>, Re<p_kc, w>, Re<p_kc, s_kc>: sigma of the next iteration
+            const float2 so = S.ss[i], po = S.pc[1][i];
+            de += (double)z.x * so.x + (double)z.y * so.y;
+            dq += (double)po.x * w.x + (double)po.y * w.y;
+            dp += (double)po.x * so.x + (double)po.y * so.y;
+          }
         }
-        {  // warp 0: W = F0 w ; warp 1: the three block sums -> partials (concurrently)
-          double v3[3] = {rz, dd, drr};
-          red_warps<3>(v3, S.red);
+        {  // warp 0: W = F0 w ; warp 1: the block sums -> partials (concurrently)
+          double v5[6] = {rz, dd, drr, de, dq, dp};
+          red_warps<6>(v5, S.red);
           if (tid < 32) {
             kr_col_fwd<M>(S.qs, a.Qs, xl, twr, boff, t);
           } else if (tid < 64) {
-            red_final<3>(S.red, v3);
+            red_final<6>(S.red, v5);
             if (tid == 32) {
-              part[t] = v3[0];
-              part[P + t] = v3[1];
-              part[2 * P + t] = v3[2];
+#pragma unroll
+              for (int q = 0; q < 6; ++q) part[q * P + t] = v5[q];
             }
           }
         }
         seg(2);
         pbar(barc, target, P);
         seg(3);
-        psum<P, 3>(part, S.bc);
-        const double rho = S.bc[0], delta = S.bc[1], rr = S.bc[2];
+        psum<P, 6>(part, S.bc);
+        const double rho = S.bc[0], delta = S.bc[1], rr = S.bc[2], zs_ = S.bc[3], pw_ = S.bc[4], ps_ = S.bc[5];
         if (kc >= 1) {  // checks of iteration kc (fin_rr, fin_rho order)
           sc.rr = rr;
           sc.iter = kc;
@@ -600,9 +605,13 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
           sc.status = ST_NONFINITE;
           break;
         }
-        // ---- iteration k = kc + 1: beta_k, sigma_k = <p_k, A p_k>, alpha_k
+        // ---- iteration k = kc + 1: beta_k, sigma_k = <p_k, A p_k>, alpha_k.  sigma is the
+        // bilinear expansion of <z + beta p, w + beta s> (s = A p from its recurrence):
+        // delta + beta (Re<z, s> + Re<p, w>) + beta^2 <p, s>, not the classical C-G identity
+        // delta - beta rho / alpha, which assumes exact orthogonality and goes non-positive
+        // once a fixed-count solve reaches the fp32 rounding floor.
         const double beta = kc == 0 ? 0.0 : rho / rho_prev;
-        const double sigma = kc == 0 ? delta : delta - beta * rho / sc.alpha;
+        const double sigma = kc == 0 ? delta : delta + beta * (zs_ + pw_) + beta * beta * ps_;
         sc.sigma = sigma;
         if (!isfinite(sigma)) {
           sc.status = ST_NONFINITE;

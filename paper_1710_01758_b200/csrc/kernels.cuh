@@ -162,7 +162,7 @@ struct KrArgs {
   float2* Qs;                // [B][M][N] column spectrum of q (rows = spectral index)
   float2* Sr;                // [B][M][N] column spectrum of r
   float2* Tb;                // [B][N][M] row-phase output, column-major
-  double* part;              // [B][3][P] block partials
+  double* part;              // [B][8][P] block partials (B * 8 * P <= B * P.cap)
   unsigned* bar;             // [B] barrier counters (zero at launch)
   unsigned long long* stamp; // [32] stage cycle counters (nullable); [8, 20) loop segments
   int prof;                  // 1: also time the PCG loop's segments (SBPCG_KR_PROF=1)
