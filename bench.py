@@ -572,6 +572,10 @@ def mask_desc(spec):
 
 
 def run_ours(args):
+    # reading A24: a fixed reduction order for the coil-sharded all-reduce (a pinned ring); set
+    # before any NCCL communicator (torch's or the library's) reads the environment
+    os.environ.setdefault("NCCL_ALGO", "Ring")
+    os.environ.setdefault("NCCL_PROTO", "Simple")
     import torch
     ws, rank, local = dist_setup()
     dist = None

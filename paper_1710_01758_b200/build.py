@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libsbpcg.so")
-SOURCES = ["sbpcg.cu", "k_matvec.cu", "k_passes.cu", "k_lambda.cu", "k_sb.cu", "k_plane.cu", "k_plane3.cu", "k_coil.cu", "k_prep.cu", "k_wav.cu", "k_pcgc.cu", "k_persist.cu"]
+SOURCES = ["sbpcg.cu", "k_matvec.cu", "k_passes.cu", "k_lambda.cu", "k_sb.cu", "k_plane.cu", "k_plane3.cu", "k_coil.cu", "k_prep.cu", "k_wav.cu", "k_persist.cu"]
 HEADERS = ["fft_core.cuh", "internal.cuh", "kernels.cuh", "pcg_fin.cuh", "sb_tile.cuh", "k_plane.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
   constexpr uint32_t XROWS = (uint32_t)(KB * NZP * sizeof(float2));  // one bulk copy: KB tile rows
 
   const int g = blockIdx.x;  // cluster rank (cluster dims = (G,1,1), grid.x = G)
-  const int xpl = blockIdx.y;
+  const int xpl = blockIdx.y + a.plane0;  // plane (launches may cover a chunk of planes)
   const int b = blockIdx.z;
   const int tid = threadIdx.x;
   const int r = tid / N2, j = tid % N2;  // row stage
@@ -674,7 +674,7 @@ static cudaError_t kp_launch(const KPArgs& a, cudaStream_t st) {
       return e;
     attr_done = true;
   }
-  return launch_ex(kern, dim3(G, a.planes, a.B), dim3(P::T), smem, st, G > 1 ? G : 0, a);
+  return launch_ex(kern, dim3(G, a.nplanes > 0 ? a.nplanes : a.planes, a.B), dim3(P::T), smem, st, G > 1 ? G : 0, a);
 }
 
 // cluster size per plane height: the column DFT holds NY/G <= 32 values and G | NY/G

@@ -123,19 +123,6 @@ struct SbArgs {
   float2* bz_out;
 };
 
-// Persistent per-problem cluster PCG (k_pcgc.cu): 256 x 256 line-mask problems, circulant M.
-struct KcArgs {
-  int B, C, N;
-  float mu, lam, gam;
-  const float* rmask;      // [B or 1][M] = r/M
-  int rmask_bstride;
-  const float* lam_inv;    // [B][M][N] = 1/(N k)
-  float2 *x, *r, *z, *pbuf0, *pbuf1, *tmp;
-  const float2* tw;        // [M] forward twiddles
-  Loop L;
-};
-bool kc_supported(int M, int N);
-cudaError_t launch_kc(const KcArgs& a, const CUtensorMap* tmap16, cudaStream_t st);
 
 // Persistent whole-GPU reconstruction / solve for small batches of square line-mask problems
 // (k_persist.cu): one cooperative launch; CTA t of problem b owns image column
@@ -222,6 +209,8 @@ struct KPArgs {
   // all-reduce the epilogue kernel (k_coil.cu) reads the reduced sum from acc_in.
   float2* acc_out;
   const float2* acc_in;
+  int plane0;                // first plane of this launch (coil mode: plane chunks overlap the
+  int nplanes;               // all-reduce of the previous chunk); nplanes = 0: all planes
   int rss_raw;               // ADJOINT: out2 = sum_c |.|^2 (no sqrt; all-reduced first)
   Loop L;
   Partials P;

@@ -98,6 +98,15 @@ struct sb_ctx {
   double k1_bytes = 0;          // algorithmic bytes per problem-launch of the matvec
   sb_comm* comm = nullptr;      // coil-sharded mode (this context holds a coil shard)
   float2* accbuf = nullptr;     // [B][img] partial / all-reduced coil sum
+  cudaStream_t cst = nullptr;   // coil mode: the all-reduce stream (overlaps the plane kernel)
+  int coil_chunks = 4;          // coil mode: plane chunks per matvec (SBPCG_COIL_CHUNKS)
+  cudaEvent_t chunk_ev[16] = {};  // coil mode: chunk k's partial sums written / all-reduced
+  cudaEvent_t red_done = nullptr;
+  cudaGraphExec_t coil_exec[4][3] = {};  // coil mode [kind: solve, recon first, next par 0/1][0 pre, 1 body, 2 post]
+  cudaGraph_t coil_graph[4][3] = {};
+  int coil_unroll = 4;          // coil mode: PCG iterations per graph launch (host check between)
+  float coil_eps = -1.f;
+  int coil_maxit = -1, coil_pre = -1;
   float* jinv = nullptr;        // Jacobi: 1/diag(A) [B][img] (built on first use)
   int wavelet = 0;              // 0 Haar (reading A6), 1 Daubechies-4 (reading A32)
   float2* wbuf = nullptr;       // D4 coefficients [B][img]
@@ -134,8 +143,6 @@ struct sb_ctx {
   float* log_relres = nullptr;
   int log_cap = 0;
   CUtensorMap tmap;
-  CUtensorMap tmap16;           // 16-column coil-map boxes for the persistent cluster PCG (KC)
-  bool kc = false;              // KC enabled: 256x256 line masks, single GPU (k_pcgc.cu)
   // graphs: 0 = solve, 1 = recon first, 2/3 = recon next (parity)
   GraphSlot gs[4];
   sb_status sticky = SB_OK;
@@ -360,44 +367,6 @@ static sb_status run_kp(sb_ctx* c, int mode, const KPArgs& a, cudaStream_t st) {
   return SB_OK;
 }
 
-// The whole PCG loop of every problem in one persistent launch (one 16-CTA cluster per
-// problem); timed like K1 for the roofline, units = PCG iterations (counted by the kernel).
-static sb_status run_kc(sb_ctx* c, Loop L, cudaStream_t st) {
-  KcArgs a;
-  memset(&a, 0, sizeof(a));
-  a.B = c->B;
-  a.C = c->C;
-  a.N = c->N;
-  a.mu = c->mu;
-  a.lam = c->lam;
-  a.gam = c->gam;
-  a.rmask = c->rowmask;
-  a.rmask_bstride = c->mask_shared ? 0 : c->M;
-  a.lam_inv = c->lam_inv;
-  a.x = c->x;
-  a.r = c->r;
-  a.z = c->z;
-  a.pbuf0 = c->p0;
-  a.pbuf1 = c->p1;
-  a.tmp = c->tmp;
-  a.tw = c->tw_m;
-  a.L = L;
-  int e0 = -1;
-  if (c->timing) {
-    CK(launch_spin(st, 20000));
-    e0 = (int)c->evnext;
-    CK(cudaEventRecord(ev_get(c), st));
-  }
-  CK(launch_kc(a, &c->tmap16, st));
-  if (c->timing) {
-    int e1 = (int)c->evnext;
-    CK(cudaEventRecord(ev_get(c), st));
-    c->evpend.push_back({0, {e0, e1}});
-  }
-  c->launches++;
-  return SB_OK;
-}
-
 static sb_status run_pass(sb_ctx* c, int kind, const PassArgs& a, cudaStream_t st) {
   CK(launch_pass(kind, a, st));
   c->launches++;
@@ -465,12 +434,32 @@ static sb_status allreduce(sb_ctx* c, void* buf, size_t count, int dtype, cudaSt
   return SB_OK;
 }
 
-// Coil-sharded matvec: plane kernel up to the partial coil sum, all-reduce, epilogue.
+// Coil-sharded matvec: the plane kernel up to the partial coil sum, in plane chunks on the
+// context stream; each chunk's NCCL all-reduce runs on the comm stream as soon as the chunk is
+// written (event dependency), so the reduction of chunk k overlaps the transforms of chunk k+1;
+// then the epilogue.  The fork/join through events also captures into CUDA graphs.
 static sb_status run_kp_sharded(sb_ctx* c, int mode, KPArgs k, cudaStream_t st) {
   k.acc_out = c->accbuf;
-  sb_status s = run_kp(c, mode, k, st);
-  if (s) return s;
-  if ((s = allreduce(c, c->accbuf, 2 * (size_t)c->B * c->img, NCCL_FLOAT32, st))) return s;
+  const int planes = k.planes;
+  const int nch = std::max(1, std::min(std::min(c->coil_chunks, 16), planes));
+  sb_status s;
+  for (int ch = 0; ch < nch; ++ch) {
+    const int p0 = (int)((int64_t)planes * ch / nch), p1 = (int)((int64_t)planes * (ch + 1) / nch);
+    if (p1 <= p0) continue;
+    KPArgs kc = k;
+    kc.plane0 = p0;
+    kc.nplanes = p1 - p0;
+    if ((s = run_kp(c, mode, kc, st))) return s;
+    CK(cudaEventRecord(c->chunk_ev[ch], st));
+    CK(cudaStreamWaitEvent(c->cst, c->chunk_ev[ch], 0));
+    const size_t pn = (size_t)k.NY * k.NZ;
+    for (int b = 0; b < c->B; ++b) {
+      float2* base = c->accbuf + (size_t)b * c->img + (size_t)p0 * pn;
+      if ((s = allreduce(c, base, 2 * (size_t)(p1 - p0) * pn, NCCL_FLOAT32, c->cst))) return s;
+    }
+  }
+  CK(cudaEventRecord(c->red_done, c->cst));
+  CK(cudaStreamWaitEvent(st, c->red_done, 0));
   k.acc_out = nullptr;
   k.acc_in = c->accbuf;
   CK(launch_kc_epilogue(mode, k, st));
@@ -705,10 +694,9 @@ static sb_status build_graph(sb_ctx* c, int kind, const sb_pcg_opts* o, const fl
   }
   cudaGraph_t G;
   CK(cudaGraphCreate(&G, 0));
-  const bool kcp = c->kc && o->precond == 1;  // persistent cluster PCG: no conditional node
   cudaGraphConditionalHandle h = 0;
-  if (!kcp) CK(cudaGraphConditionalHandleCreate(&h, G, 0, 0));
-  Loop L = make_loop(c, kcp ? 0ull : (unsigned long long)h);
+  CK(cudaGraphConditionalHandleCreate(&h, G, 0, 0));
+  Loop L = make_loop(c, (unsigned long long)h);
   cudaStream_t cs = c->cap1;
   int64_t l0 = c->launches;
   bool saved_timing = c->timing;
@@ -736,26 +724,6 @@ static sb_status build_graph(sb_ctx* c, int kind, const sb_pcg_opts* o, const fl
     cudaStreamEndCapture(cs, &dummy);
     c->timing = saved_timing;
     return s;
-  }
-  if (kcp) {
-    const int64_t lb = c->launches;
-    s = run_kc(c, L, cs);
-    if (!s) s = seq_post(c, L, cs);
-    cudaGraph_t Gout;
-    cudaError_t e3 = cudaStreamEndCapture(cs, &Gout);
-    c->timing = saved_timing;
-    if (s) return s;
-    CK(e3);
-    CK(cudaGraphInstantiate(&g.exec, G, 0));
-    g.graph = G;
-    g.nbody = 0;
-    g.nfixed = (int)(c->launches - l0);
-    (void)lb;
-    c->launches = l0;
-    g.eps = o->eps;
-    g.maxit = o->max_iters;
-    g.precond = o->precond;
-    return SB_OK;
   }
   cudaStreamCaptureStatus cst;
   const cudaGraphNode_t* deps = nullptr;
@@ -841,10 +809,6 @@ static sb_status eager_solve(sb_ctx* c, int kind, const sb_pcg_opts* o, const fl
     ~Closer() { m.close(); }
   } closer{mp};
   if ((s = seq_precond(c, L, o->precond, 0, c->r, c->z, st))) return s;
-  if (c->kc && o->precond == 1) {  // persistent cluster PCG
-    if ((s = run_kc(c, L, st))) return s;
-    return seq_post(c, L, st);
-  }
   int host_any = 1;
   CK(cudaMemcpyAsync(&host_any, &c->ctl->any_active, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -856,7 +820,130 @@ static sb_status eager_solve(sb_ctx* c, int kind, const sb_pcg_opts* o, const fl
   return seq_post(c, L, st);
 }
 
+// Coil-sharded mode in CUDA graphs (the NCCL all-reduces and the comm-stream fork/join are
+// captured): [prelude] once, then [U PCG iterations] per launch with one host check of the
+// "any problem active" flag between launches (a conditional node cannot hold the NCCL work),
+// then [fixup + log].  Every rank sees the same flags (bitwise identical replicated scalars), so
+// every rank launches the same collectives.
+static void coil_graphs_drop(sb_ctx* c) {
+  for (auto& row : c->coil_exec)
+    for (auto& e : row)
+      if (e) {
+        cudaGraphExecDestroy(e);
+        e = nullptr;
+      }
+  for (auto& row : c->coil_graph)
+    for (auto& g : row)
+      if (g) {
+        cudaGraphDestroy(g);
+        g = nullptr;
+      }
+  c->coil_maxit = -1;
+}
+
+template <typename F>
+static sb_status capture(sb_ctx* c, F&& body, cudaGraph_t* g, cudaGraphExec_t* e) {
+  cudaStream_t cs = c->cap1;
+  CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  sb_status s = body(cs);
+  cudaGraph_t gr = nullptr;
+  cudaError_t ec = cudaStreamEndCapture(cs, &gr);
+  if (s) {
+    if (gr) cudaGraphDestroy(gr);
+    return s;
+  }
+  CK(ec);
+  CK(cudaGraphInstantiate(e, gr, 0));
+  *g = gr;
+  return SB_OK;
+}
+
+static sb_status coil_graph_solve(sb_ctx* c, int kind, const sb_pcg_opts* o, const float2* ydev) {
+  if (c->coil_eps != o->eps || c->coil_maxit != o->max_iters || c->coil_pre != o->precond) {
+    coil_graphs_drop(c);
+    c->coil_eps = o->eps;
+    c->coil_maxit = o->max_iters;
+    c->coil_pre = o->precond;
+  }
+  const bool saved_timing = c->timing;
+  c->timing = false;
+  struct PdlGuard {
+    bool old;
+    PdlGuard() : old(g_use_pdl) { g_use_pdl = false; }
+    ~PdlGuard() { g_use_pdl = old; }
+  } pdl_guard;
+  Loop L = make_loop(c, 0ull);
+  sb_status s = SB_OK;
+  const int64_t l0 = c->launches;
+  int n_pre = 0, n_body = 0, n_post = 0;
+  if (!c->coil_exec[kind][0]) {
+    s = capture(c, [&](cudaStream_t cs) -> sb_status {
+      sb_status r;
+      if (kind == 0) {
+        r = seq_resid(c, L, c->bvec, false, false, false, o->eps, o->max_iters, cs);
+      } else if (kind == 1) {
+        r = seq_init_recon(c, ydev, cs);
+        if (!r) r = seq_resid(c, L, nullptr, true, false, false, o->eps, o->max_iters, cs);
+      } else {
+        r = seq_shrink(c, kind - 2, cs);
+        if (!r) r = seq_resid(c, L, nullptr, true, true, true, o->eps, o->max_iters, cs);
+      }
+      if (!r) r = seq_precond(c, L, o->precond, 0, c->r, c->z, cs);
+      return r;
+    }, &c->coil_graph[kind][0], &c->coil_exec[kind][0]);
+    if (!s)
+      s = capture(c, [&](cudaStream_t cs) -> sb_status {
+        for (int u = 0; u < c->coil_unroll; ++u) {
+          sb_status r = seq_body(c, L, o->precond, cs, nullptr);
+          if (r) return r;
+        }
+        return SB_OK;
+      }, &c->coil_graph[kind][1], &c->coil_exec[kind][1]);
+    if (!s)
+      s = capture(c, [&](cudaStream_t cs) -> sb_status { return seq_post(c, L, cs); }, &c->coil_graph[kind][2],
+                  &c->coil_exec[kind][2]);
+  }
+  (void)n_pre, (void)n_body, (void)n_post;
+  c->launches = l0;  // capture does not launch
+  c->timing = saved_timing;
+  if (s) {
+    coil_graphs_drop(c);
+    return s;
+  }
+  auto kernel_nodes = [](cudaGraph_t g) -> int64_t {
+    size_t n = 0;
+    if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess) return 0;
+    std::vector<cudaGraphNode_t> nodes(n);
+    if (n == 0 || cudaGraphGetNodes(g, nodes.data(), &n) != cudaSuccess) return 0;
+    int64_t k = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+    }
+    return k;
+  };
+  int64_t nn = kernel_nodes(c->coil_graph[kind][0]);
+  c->launches += nn;
+  CK(cudaGraphLaunch(c->coil_exec[kind][0], c->st));
+  int host_any = 1;
+  CK(cudaMemcpyAsync(&host_any, &c->ctl->any_active, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  nn = kernel_nodes(c->coil_graph[kind][1]);
+  while (host_any) {
+    CK(cudaGraphLaunch(c->coil_exec[kind][1], c->st));
+    c->launches += nn;
+    CK(cudaMemcpyAsync(&host_any, &c->ctl->any_active, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  }
+  nn = kernel_nodes(c->coil_graph[kind][2]);
+  c->launches += nn;
+  CK(cudaGraphLaunch(c->coil_exec[kind][2], c->st));
+  c->last_path = SB_PATH_COIL_SHARDED;
+  return SB_OK;
+}
+
 static sb_status run_solve_kind(sb_ctx* c, int kind, const sb_pcg_opts* o, const float2* ydev) {
+  if (c->comm && o->use_graph && !c->timing && !c->stage_timing) return coil_graph_solve(c, kind, o, ydev);
   // coil-sharded mode runs the host-driven loop; stage timers need the eager sequence
   if (o->use_graph && !c->timing && !c->comm && !c->stage_timing) {
     sb_status s = build_graph(c, kind, o, ydev);
@@ -871,7 +958,7 @@ static sb_status run_solve_kind(sb_ctx* c, int kind, const sb_pcg_opts* o, const
 
 // ------------------------------------------------------------------ persistent kernel (KR)
 static bool use_kr(sb_ctx* c, const sb_pcg_opts* o) {
-  return c->kr_ok && c->kr_on && o->precond == 1 && c->wavelet == 0 && !c->comm && !c->kc;
+  return c->kr_ok && c->kr_on && o->precond == 1 && c->wavelet == 0 && !c->comm;
 }
 
 // One cooperative launch: n_outer = 0 solves A x = b (b in c->bvec, x0 in c->x); n_outer >= 1
@@ -1179,6 +1266,16 @@ void sb_pcg_destroy(sb_ctx* c) {
   }
   for (auto e : c->evpool) cudaEventDestroy(e);
   for (auto e : c->stage_pool) cudaEventDestroy(e);
+  for (auto e : c->chunk_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->red_done) cudaEventDestroy(c->red_done);
+  for (auto& row : c->coil_exec)
+    for (auto& e : row)
+      if (e) cudaGraphExecDestroy(e);
+  for (auto& row : c->coil_graph)
+    for (auto& g : row)
+      if (g) cudaGraphDestroy(g);
+  if (c->cst) cudaStreamDestroy(c->cst);
   void* bufs[] = {c->sens, c->mask, c->rowmask, c->lam_inv, c->kbuf, c->tw_m, c->tw_n, c->twd_m, c->twd_n,
                   c->x, c->r, c->z, c->q, c->p0, c->p1, c->tmp, c->bvec, c->u, c->u1, c->rhs,
                   c->bx[0], c->bx[1], c->by[0], c->by[1], c->bw, c->tmpc, c->stage_in, c->stage_out,
@@ -1404,12 +1501,6 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   c->k1_bytes = 8.0 * (double)img * c->C + 48.0 * (double)img +
                 (c->separable ? 4.0 * c->M : (double)(d3 ? (size_t)D1 * D2 : img));
   sb_status s = c->plane ? SB_OK : make_tmap(c);  // K1 streams the coil maps by TMA
-  // the persistent cluster PCG for 256x256 line-mask problems: opt-in (SBPCG_KC=1). Measured
-  // slower than the kernel sequence on B200 (config 2 18.0k vs 19.8k it/s: one 16-CTA cluster
-  // per slice runs the 12 coils serially on 16 SMs; config 3 128k vs 173k: per-slice
-  // iteration imbalance leaves clusters idle at the end of a launch)
-  c->kc = !d3 && c->separable && kc_supported(c->M, c->N) && c->C >= 1 && env_flag("SBPCG_KC", false);
-  if (!s && c->kc) s = make_tmap_w(c, &c->tmap16, 16);
   if (s) {
     sb_pcg_destroy(c);
     return s;
@@ -1437,6 +1528,20 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
       return SB_E_NOMEM;
     }
     c->comm = comm;
+  }
+  if (!s && d3) {  // the coil mode's comm stream and chunk events (also for sb_pcg_set_comm)
+    if (cudaStreamCreateWithFlags(&c->cst, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->red_done, cudaEventDisableTiming) != cudaSuccess) {
+      sb_pcg_destroy(c);
+      return SB_E_CUDA;
+    }
+    for (auto& e : c->chunk_ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+        sb_pcg_destroy(c);
+        return SB_E_CUDA;
+      }
+    if (const char* ce = getenv("SBPCG_COIL_CHUNKS")) c->coil_chunks = std::max(1, std::min(16, atoi(ce)));
+    if (const char* cu = getenv("SBPCG_COIL_UNROLL")) c->coil_unroll = std::max(1, std::min(16, atoi(cu)));
   }
   s = build_lambda(c);
   if (s) {
@@ -1477,6 +1582,10 @@ sb_status sb_comm_unique_id(void* id_out) {
 sb_status sb_comm_init(const void* id, int32_t rank, int32_t world, sb_comm** out) {
   if (!out || !id || world < 1 || rank < 0 || rank >= world) return SB_E_ARG;
   *out = nullptr;
+  // reading A24 (fixed reduction order): a pinned ring all-reduce reduces in the same order on
+  // every call; NVLS / tree selection could change it.  The caller's settings win.
+  setenv("NCCL_ALGO", "Ring", 0);
+  setenv("NCCL_PROTO", "Simple", 0);
   if (!nccl_load()) return SB_E_COMM;
   nccl_uid_t uid;
   memcpy(&uid, id, sizeof(uid));
@@ -1510,6 +1619,7 @@ sb_status sb_pcg_set_comm(sb_ctx* c, sb_comm* cm) {
   if (cm && !c->accbuf) CK(dalloc(&c->accbuf, (size_t)c->B * c->img));
   c->comm = cm;
   for (auto& g : c->gs) g.maxit = -1;  // cached graphs do not apply
+  coil_graphs_drop(c);
   return build_lambda(c);               // Lambda from the marginal over all ranks' coils
 }
 
@@ -1597,6 +1707,7 @@ sb_status sb_set_wavelet(sb_ctx* c, int32_t family) {
   if (family == 1 && !c->wbuf) CK(dalloc(&c->wbuf, (size_t)c->B * c->img));
   c->wavelet = family;
   for (auto& g : c->gs) g.maxit = -1;  // the captured shrink step changes
+  coil_graphs_drop(c);
   return SB_OK;
 }
 
@@ -1750,6 +1861,7 @@ static sb_status ensure_hist(sb_ctx* c, int maxit, int slots) {
     CK(dalloc(&c->hist, (size_t)c->B * (maxit + 1)));
     c->hist_stride = maxit + 1;
     for (auto& g : c->gs) g.maxit = -1;  // graphs captured the old pointer
+    coil_graphs_drop(c);
   }
   if (c->log_cap < slots) {
     if (c->log_iters) cudaFree(c->log_iters);
@@ -1758,6 +1870,7 @@ static sb_status ensure_hist(sb_ctx* c, int maxit, int slots) {
     CK(dalloc(&c->log_relres, (size_t)c->B * slots));
     c->log_cap = slots;
     for (auto& g : c->gs) g.maxit = -1;
+    coil_graphs_drop(c);
   }
   return SB_OK;
 }
@@ -1789,7 +1902,7 @@ sb_status sb_pcg_solve(sb_ctx* c, const sb_c64* b, sb_c64* x, const sb_pcg_opts*
     }
     timing_collect(c);
   }
-  if (o->use_graph && !c->timing && !kr) {
+  if (c->last_path == SB_PATH_GRAPH && !c->timing) {
     int mx = 0;
     for (auto& h : hs) mx = std::max(mx, h.iter);
     const GraphSlot& g0 = c->gs[0];
@@ -1896,7 +2009,7 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
     if (kr) c->kr_alg_bytes += kr_bytes(c, li, ro->n_outer, true);
     timing_collect(c);
   }
-  if (o->use_graph && !c->timing && !kr) {
+  if (c->last_path == SB_PATH_GRAPH && !c->timing) {
     for (int j = 0; j < ro->n_outer; ++j) {
       int mx = 0;
       for (int b = 0; b < c->B; ++b) mx = std::max(mx, li[(size_t)j * c->B + b]);
@@ -2000,9 +2113,7 @@ sb_status sb_get_kernel_time(sb_ctx* c, int32_t which, double* ms, int64_t* laun
     // + z, p_{k-1} (and halo), x read + x, p_k, q written (6 x 8N) + row mask (4M);
     // averaged over the timed launches using the device count of active problems.
     const double N = (double)c->img;
-    // KC (persistent PCG): one unit = one PCG iteration, B_iter = 8N(C+10) + 4N + 4M
-    const double per = which == 0 ? (c->kc ? 8.0 * N * (c->C + 10) + 4.0 * N + 4.0 * c->M : c->k1_bytes)
-                                  : (4.0 * 8.0 * N + 4.0 * N);
+    const double per = which == 0 ? c->k1_bytes : (4.0 * 8.0 * N + 4.0 * N);
     Counters h{};
     if (cudaMemcpy(&h, c->counters, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return fail(c, SB_E_CUDA, "counters");
     const double probs = (which == 0 && c->t_n[0] > 0) ? (double)h.k1_problems / (double)c->t_n[0] : (double)c->B;

@@ -1,9 +1,11 @@
 """Host-side logic of the coil-sharded mode on CPU with world_size 2 (gloo): each rank takes
-its contiguous coil shard (paper_1710_01758_b200.coil_shard, mirrored here without loading
-the CUDA library), computes its partial data term sum_{c in shard} E_c^H E_c x with the
-oracle, and one all-reduce gives the full operator — the decomposition the
-library's per-matvec NCCL all-reduce relies on; Lambda's coil marginal decomposes the same
-way (k is affine in sum_c |F s_c|^2)."""
+its contiguous coil shard (the rule of paper_1710_01758_b200.coil_shard, mirrored here for the
+spawned workers and checked equal to the binding's function below), computes its partial data
+term sum_{c in shard} E_c^H E_c x with the oracle, and one all-reduce gives the full operator
+ — the decomposition the library's per-matvec NCCL all-reduce relies on; Lambda's
+coil marginal decomposes the same way (k is affine in sum_c |F s_c|^2).
+The reference for the coil marginal g uses numpy.fft (a library FFT), so this checks the
+decomposition, not the library's FFT."""
 import os
 
 import numpy as np
@@ -17,8 +19,7 @@ from oracle import ops, precond
 
 
 def coil_shard(coils, rank, world):
-    # same rule as paper_1710_01758_b200.sbpcg.coil_shard (checked below against it when the
-    # binding is importable)
+    # same rule as paper_1710_01758_b200.sbpcg.coil_shard (test_mirror_equals_binding)
     base, extra = divmod(coils, world)
     c0 = rank * base + min(rank, extra)
     return c0, c0 + base + (1 if rank < extra else 0)
@@ -55,6 +56,15 @@ def test_coil_shard_partition():
             assert rs[0][0] == 0 and rs[-1][1] == C
             assert all(rs[i][1] == rs[i + 1][0] for i in range(W - 1))
             assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
+
+
+def test_mirror_equals_binding():
+    # the binding loads libsbpcg.so without a GPU (ctypes; no compute call is made)
+    from paper_1710_01758_b200 import coil_shard as lib_coil_shard
+    for C in (1, 5, 12, 16, 32):
+        for W in (1, 2, 3, 4, 8):
+            for r in range(W):
+                assert coil_shard(C, r, W) == lib_coil_shard(C, r, W)
 
 
 def test_coil_sharded_data_term_allreduce_world2():

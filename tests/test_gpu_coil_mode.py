@@ -1,6 +1,7 @@
 """Coil-sharded mode (SURVEY 8(e), config 5 over G GPUs) on one GPU: a world-size-1 NCCL
-communicator exercises the whole sharded data path (plane kernel partial sum -> ncclAllReduce
--> epilogue kernel, host-driven loop, all-reduced Lambda marginal / u_1 / RSS); results must
+communicator exercises the whole sharded data path (the plane kernel's partial sums in plane
+chunks -> per-chunk ncclAllReduce on the comm stream -> epilogue kernel; the loop captured in
+CUDA graphs of U iterations, or eager; all-reduced Lambda marginal / u_1 / RSS); results must
 equal the unsharded context.  The multi-rank decomposition itself is covered on CPU by
 tests/test_coil_shard_gloo.py."""
 import numpy as np
@@ -44,6 +45,35 @@ def test_coil_mode_world1_equals_unsharded():
     xb, lb = b.recon(yt, 3, eps=1e-4, max_iters=40)
     assert la["pcg_iters"] == lb["pcg_iters"]
     assert relerr(xb.cpu().numpy(), xa.cpu().numpy()) <= 1e-5
+    a.close(), b.close(), comm.close()
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+@pytest.mark.parametrize("graph", [True, False], ids=["graph", "eager"])
+def test_coil_mode_chunked_and_graph(monkeypatch, chunks, graph):
+    # comm given at create (sb_pcg_create's comm argument); chunked all-reduce; graphs or eager
+    p = synth.problem3d(5, shape=(8, 32, 32), coils=3, amplitude=100.0)
+    y = problems.make_kspace(p["phantom"], p["sens"], p["mask"], p["noise"])
+    monkeypatch.setenv("SBPCG_COIL_CHUNKS", str(chunks))
+    monkeypatch.setenv("SBPCG_COIL_UNROLL", "3")
+    comm = SbComm(SbComm.unique_id(), 0, 1)
+    a = _ctx(p)
+    b = SbPcg(torch.from_numpy(p["sens"][None]).to(torch.complex64).cuda(), torch.from_numpy(p["mask"][None]).cuda(),
+              1.0, 0.01, 0.01, 2, comm=comm)
+    yt = torch.from_numpy(y[None]).to(torch.complex64).cuda()
+    for eps, mx in ((0.0, 7), (1e-4, 40)):
+        xa, la = a.recon(yt, 3, eps=eps, max_iters=mx)
+        xb, lb = b.recon(yt, 3, eps=eps, max_iters=mx, use_graph=graph)
+        assert lb["path"] == "coil-sharded"
+        assert la["pcg_iters"] == lb["pcg_iters"]
+        assert relerr(xb.cpu().numpy(), xa.cpu().numpy()) <= 1e-5
+    # the solve entry point through the same path
+    rng = np.random.default_rng(4)
+    bb = torch.from_numpy((rng.standard_normal((1, 8, 32, 32)) + 1j * rng.standard_normal((1, 8, 32, 32)))
+                          .astype(np.complex64)).cuda()
+    xa, sa = a.solve(bb, torch.zeros_like(bb), eps=1e-5, max_iters=60)
+    xb, sb_ = b.solve(bb, torch.zeros_like(bb), eps=1e-5, max_iters=60, use_graph=graph)
+    assert sa["iters"] == sb_["iters"] and relerr(xb.cpu().numpy(), xa.cpu().numpy()) <= 1e-5
     a.close(), b.close(), comm.close()
 
 

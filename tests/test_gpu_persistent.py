@@ -129,8 +129,7 @@ def test_kr_sb_recon_fixed_counts_vs_oracle(case, amp, cg):
     ctx.close()
 
 
-@pytest.mark.parametrize("amp", [1.0, 100.0])
-@CG
+@pytest.mark.parametrize("amp,cg", [(1.0, False), (100.0, True)], ids=["std-amp1", "cg-amp100"])
 def test_kr_sb_recon_bench_shape_fixed_counts(amp, cg):
     # the exact bench shape (config 2: 256^2, 12 coils, VD lines, 3-level Haar, mu=1,
     # lam=gam=0.02), B = 1, eps = 0: 5 outer x 10 CG against the oracle
