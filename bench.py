@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--std-pcg", action="store_true", help="persistent kernel: standard PCG recurrences")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--full-cpu-baseline", action="store_true",
+                    help="oracle baseline with complete SB reconstructions (BASELINE.md §3; minutes)")
     ap.add_argument("--no-extra", action="store_true", help="skip the configs 3-5 extra measurements")
     ap.add_argument("--extra", default="3,4,5", help="configs measured in the extra object")
     ap.add_argument("--slices", type=int, default=0, help="override problems per rank")
@@ -262,21 +264,22 @@ def cpu_baseline_3d(cfg, precond):
                       f"iteration at 192^3 (numpy fp64, own FFT; coil terms in parallel over the cores)"}
 
 
-def cpu_baseline(cfg, precond):
-    """The oracle on all host cores: configs 1-2 run FULL SB reconstructions,
-    one independent slice per core; configs 3-4 run 2 outer iterations of one slice per core
-    (the batch is independent slices, so slices/s scale with cores); config 5 extrapolates."""
+def cpu_baseline(cfg, precond, full=False):
+    """The oracle on all host cores, one independent slice per core (single-threaded numpy
+    processes): by default a bounded sample of 2 SB outer iterations per slice (~10-15 s);
+    `full` (--full-cpu-baseline) runs complete SB reconstructions (~100 s for
+    config 2).  Config 5 extrapolates from one coil's data-term pair."""
     if cfg == 5:
         return cpu_baseline_3d(cfg, precond)
     spec = synth.CONFIGS[cfg]
     cores = os.cpu_count() or 1
-    n_outer = spec.params.n_outer if cfg in (1, 2) else 2
+    n_outer = spec.params.n_outer if full else 2
     jobs = [(cfg, s, n_outer, precond) for s in range(cores)]
     wall, its, per, procs = _oracle_pool(jobs)
     return {"value": its / wall, "unit": "PCG iters/s", "cores": procs, "kind": "oracle", "cpu": cpu_model(),
             "sb_recon_s": statistics.median(per),
             "sample": f"{procs} independent slices in parallel, one single-threaded numpy fp64 process per core, "
-                      f"{n_outer} SB outer iterations each ({'full reconstruction' if cfg in (1, 2) else 'partial'}); "
+                      f"{n_outer} SB outer iterations each ({'full reconstruction' if n_outer == spec.params.n_outer else 'partial'}); "
                       f"{its} PCG iterations in {wall:.1f} s wall; median per-slice sb_recon {statistics.median(per):.1f} s"}
 
 
@@ -610,7 +613,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.config, args.precond)
+        cpu = cpu_baseline(args.config, args.precond, full=args.full_cpu_baseline)
 
     if rank == 0:
         prm = spec.params
