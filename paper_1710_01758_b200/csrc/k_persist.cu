@@ -65,6 +65,8 @@ struct KrSmem {
   float2 srow[M];                     // row t of S_r = F_0 r
   float2 ss[M];                       // s = A p, own column (Chronopoulos-Gear loop)
   float2 ssrow[M];                    // row t of S_s = F_0 s (Chronopoulos-Gear loop)
+  float2 wrow[M];                     // row t of W = F_0 w (cp.async prefetch after the barrier)
+  float2 ub[M], u1b[M], rhb[M];       // prelude: u, u1, rhs_reg (or b) of the own column
   float2 tw[M];
   float li[M];                        // Lambda^{-1} of spectral row t
   float rm[M];                        // r/M (row mask)
@@ -90,6 +92,12 @@ __device__ __forceinline__ void red_relaxed(unsigned* p, unsigned v) {
   asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+__device__ __forceinline__ void kr_cp16(void* dst, const void* src) {  // 16-byte global -> shared, L2 only
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void kr_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void kr_cp_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // A barrier that has not completed after ~4 s traps (a bug must fail the launch, not hang it).
 __device__ __noinline__ void pbar_stuck(const unsigned* ctr, unsigned target) {
@@ -441,13 +449,30 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
     sc.active = 1;
 
     // ================= prelude: r0 = b - A x0 (+ RHS and data feedback) ; S_r = F0 r0
-    {
-      constexpr int E = (3 * M + NT - 1) / NT;
-      float2 xv[E];
+    seg(-1);
+    {  // one load batch: x of columns t-1, t, t+1 and u, u1, rhs_reg (or b) of column t
+      constexpr int E = (3 * M + NT - 1) / NT, EO = (M + NT - 1) / NT;
+      float2 xv[E], uv[EO], u1v[EO], rv[EO];
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         const int e = tid + k * NT;
         if (e < 3 * M) xv[k] = __ldcg(a.x + boff + (size_t)(e % M) * N + (t + e / M - 1 + N) % N);
+      }
+#pragma unroll
+      for (int k = 0; k < EO; ++k) {
+        const int i = tid + k * NT;
+        if (i < M) {
+          const size_t gi = boff + (size_t)i * N + t;
+          if (recon) {
+            uv[k] = __ldcg(a.u + gi);
+            if (update_u) {
+              u1v[k] = __ldcg(a.u1 + gi);
+              rv[k] = __ldcg(a.rhs + gi);
+            }
+          } else {
+            rv[k] = __ldcg(a.bvec + gi);
+          }
+        }
       }
 #pragma unroll
       for (int k = 0; k < E; ++k) {
@@ -457,9 +482,26 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
           if (e / M == 1) S.xs[e % M] = xv[k];
         }
       }
+#pragma unroll
+      for (int k = 0; k < EO; ++k) {
+        const int i = tid + k * NT;
+        if (i < M) {
+          if (recon) {
+            S.ub[i] = uv[k];
+            if (update_u) {
+              S.u1b[i] = u1v[k];
+              S.rhb[i] = rv[k];
+            }
+          } else {
+            S.rhb[i] = rv[k];
+          }
+        }
+      }
     }
     __syncthreads();
+    seg(10);
     kr_dataterm<M, SMC>(S, S.pc[1], coils, sTb, C, xl, twr);
+    seg(11);
     double d0 = 0.0, d1 = 0.0;
     for (int i = tid; i < M; i += NT) {
       const size_t gi = boff + (size_t)i * N + t;
@@ -468,16 +510,16 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
       const float2 reg = lap_reg(i, xc);
       float2 bb;
       if (recon) {
-        float2 uu = __ldcg(a.u + gi);
+        float2 uu = S.ub[i];
         if (update_u) {  // u_{j+1} = u_j + u_1 - E^H E x (reading A28)
-          const float2 u1 = __ldcg(a.u1 + gi);
+          const float2 u1 = S.u1b[i];
           uu = make_float2(uu.x + u1.x - av.x, uu.y + u1.y - av.y);
           a.u[gi] = uu;
         }
-        const float2 rr = update_u ? __ldcg(a.rhs + gi) : make_float2(0.f, 0.f);
+        const float2 rr = update_u ? S.rhb[i] : make_float2(0.f, 0.f);
         bb = make_float2(a.mu * uu.x + rr.x, a.mu * uu.y + rr.y);
       } else {
-        bb = __ldcg(a.bvec + gi);
+        bb = S.rhb[i];
       }
       const float2 r = make_float2(bb.x - (a.mu * av.x + reg.x), bb.y - (a.mu * av.y + reg.y));
       S.rs[i] = r;
@@ -491,7 +533,9 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
       part[t] = d0;
       part[P + t] = d1;
     }
+    seg(12);
     pbar(barc, target, P);
+    seg(13);
     psum<P, 2>(part, S.bc);
     {
       const double nb2 = S.bc[0], rr = S.bc[1];
@@ -518,6 +562,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
         }
       }
     }
+    seg(14);
     stamp(0);
 
     if (sc.active && a.cg) {
@@ -574,6 +619,9 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
         seg(2);
         pbar(barc, target, P);
         seg(3);
+        // row t of W: its L2 round trip overlaps the all-reduce read (cp.async, no registers)
+        for (int e = tid; e < N / 2; e += NT) kr_cp16(S.wrow + 2 * e, a.Qs + boff + (size_t)t * N + 2 * e);
+        kr_cp_commit();
         psum<P, 6>(part, S.bc);
         const double rho = S.bc[0], delta = S.bc[1], rr = S.bc[2], zs_ = S.bc[3], pw_ = S.bc[4], ps_ = S.bc[5];
         if (kc >= 1) {  // checks of iteration kc (fin_rr, fin_rho order)
@@ -644,12 +692,13 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
           S.rs[i] = make_float2(r0.x - fa * sv.x, r0.y - fa * sv.y);
         }
         // row t: S_s = W + beta S_s ; S_r -= alpha S_s ; T = F1^H Lambda^{-1} F1 S_r
+        kr_cp_wait();
+        __syncthreads();  // every thread's part of the W row has landed
         if (tid < 32) {
           constexpr int N1_ = N1;
           float2 v[N1_];
-          const float2* wr = a.Qs + boff + (size_t)t * N;
 #pragma unroll
-          for (int n1 = 0; n1 < N1_; ++n1) v[n1] = __ldcg(wr + N2 * n1 + j);
+          for (int n1 = 0; n1 < N1_; ++n1) v[n1] = S.wrow[N2 * n1 + j];
 #pragma unroll
           for (int n1 = 0; n1 < N1_; ++n1) {
             const int i = N2 * n1 + j;
@@ -822,6 +871,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
     }
 
     // ================= solve exit: x (own column) to the image, scalars and log
+    seg(-1);
     for (int i = tid; i < M; i += NT)
       a.x[boff + (size_t)i * N + t] = sc.zero_x ? make_float2(0.f, 0.f) : S.xs[i];
     if (lead && tid == 0) {
@@ -846,7 +896,9 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
     if (!recon) break;
 
     // ================= SB step (Alg. 1 steps 6-11 and the regulariser RHS), 16 x 16 tiles
+    seg(15);
     pbar(barc, target, P);  // x of every column visible
+    seg(16);
     {
       SbArgs sa = a.sb;
       const int par = js & 1;
@@ -858,7 +910,9 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
       const int ntj = N / TT, ntile = (M / TT) * ntj;
       for (int tile = t; tile < ntile; tile += P) sb_tile<TT, true, NT>(sa, S.u.sb, tile / ntj, tile % ntj, b);
     }
+    seg(17);
     pbar(barc, target, P);  // rhs_reg, b_* visible to the next prelude
+    seg(18);
     stamp(2);
   }
   if (timer) {

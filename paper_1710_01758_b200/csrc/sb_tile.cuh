@@ -47,25 +47,91 @@ __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, 
   const bool do_tv = a.lam != 0.f, do_w = a.gam != 0.f;
   const float tl = do_tv ? 1.f / a.lam : 0.f, tg = do_w ? 1.f / a.gam : 0.f;
 
-  for (int e = tid; e < (TH + 2) * (TW + 2); e += nt) {
-    const int u = e / (TW + 2), v = e % (TW + 2);
-    const int gi = (i0 + u - 1 + M) % M, gj = (j0 + v - 1 + N) % N;
-    xs[u][v] = __ldcg(a.x + boff + (size_t)gi * N + gj);
+  // Mallat position (in the image) of the tile's coefficient (u, v) after L levels
+  auto mallat_gi = [&](int u, int v) -> size_t {
+    int lv = 1, hi0 = 0, hi1 = 0, ca = u, cb = v;
+    bool ll = true;
+    for (; lv <= L; ++lv) {
+      const int h0 = TH >> lv, h1 = TW >> lv;
+      if (u < h0 && v < h1) continue;
+      hi0 = u >= h0;
+      hi1 = v >= h1;
+      ca = u - hi0 * h0;
+      cb = v - hi1 * h1;
+      ll = false;
+      break;
+    }
+    int gu, gv;
+    if (ll) {
+      gu = (i0 >> L) + u;
+      gv = (j0 >> L) + v;
+    } else {
+      gu = (hi0 ? (M >> lv) : 0) + (i0 >> lv) + ca;
+      gv = (hi1 ? (N >> lv) : 0) + (j0 >> lv) + cb;
+    }
+    return boff + (size_t)gu * N + gv;
+  };
+
+  // every global load of the tile issued in one batch (x with a one-pixel halo, the old b_x /
+  // b_y with their halo row / column, b_w at the tile's Mallat positions), then staged: one L2
+  // round trip instead of three
+  constexpr int KX = ((TT + 2) * (TT + 2) + nt - 1) / nt, KV = ((TT + 1) * TT + nt - 1) / nt;
+  constexpr int KB = (TT * TT + nt - 1) / nt;
+  float2 rx[KX], rvx[KV], rvy[KV], rbw[KB];
+#pragma unroll
+  for (int k = 0; k < KX; ++k) {
+    const int e = tid + k * nt;
+    if (e < (TH + 2) * (TW + 2)) {
+      const int u = e / (TW + 2), v = e % (TW + 2);
+      const int gi = (i0 + u - 1 + M) % M, gj = (j0 + v - 1 + N) % N;
+      rx[k] = __ldcg(a.x + boff + (size_t)gi * N + gj);
+    }
+  }
+  if (do_tv) {
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+      const int e = tid + k * nt;
+      if (e < (TH + 1) * TW) {
+        const int u = e / TW, v = e % TW;
+        rvx[k] = __ldcg(a.bx_in + boff + (size_t)((i0 + u) % M) * N + j0 + v);
+      }
+      if (e < TH * (TW + 1)) {
+        const int u = e / (TW + 1), v = e % (TW + 1);
+        rvy[k] = __ldcg(a.by_in + boff + (size_t)(i0 + u) * N + (j0 + v) % N);
+      }
+    }
+  }
+  if (do_w) {
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+      const int e = tid + k * nt;
+      if (e < TH * TW) rbw[k] = __ldcg(a.bw + mallat_gi(e / TW, e % TW));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KX; ++k) {
+    const int e = tid + k * nt;
+    if (e < (TH + 2) * (TW + 2)) xs[e / (TW + 2)][e % (TW + 2)] = rx[k];
+  }
+  if (do_tv) {
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+      const int e = tid + k * nt;
+      if (e < (TH + 1) * TW) vx[e / TW][e % TW] = rvx[k];
+      if (e < TH * (TW + 1)) vy[e / (TW + 1)][e % (TW + 1)] = rvy[k];
+    }
+  }
+  if (do_w) {  // the old b_w, coefficient order, parked in wv until the shrink
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+      const int e = tid + k * nt;
+      if (e < TH * TW) wv[e / TW][e % TW] = rbw[k];
+    }
   }
   __syncthreads();
 
   if (do_tv) {
     // v_x at rows i0..i0+TH (TH+1), cols j0..j0+TW-1 ; v_y at rows i0..i0+TH-1, cols j0..j0+TW
-    // stage the old b_x / b_y tiles (+1 halo) in shared memory first: loads only
-    for (int e = tid; e < (TH + 1) * TW; e += nt) {
-      const int u = e / TW, v = e % TW;
-      vx[u][v] = __ldcg(a.bx_in + boff + (size_t)((i0 + u) % M) * N + j0 + v);
-    }
-    for (int e = tid; e < TH * (TW + 1); e += nt) {
-      const int u = e / (TW + 1), v = e % (TW + 1);
-      vy[u][v] = __ldcg(a.by_in + boff + (size_t)(i0 + u) * N + (j0 + v) % N);
-    }
-    __syncthreads();
     for (int e = tid; e < (TH + 1) * TW; e += nt) {
       const int u = e / TW, v = e % TW;
       const int gi = (i0 + u) % M, gj = j0 + v;
@@ -124,31 +190,12 @@ __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, 
         __syncthreads();
       }
     }
-    // shrink in the coefficient domain, b_w update at global Mallat positions
+    // shrink in the coefficient domain, b_w update at global Mallat positions (the old b_w was
+    // parked in wv by the load batch; each thread reads and overwrites only its own cells)
     for (int e = tid; e < TH * TW; e += nt) {
       const int u = e / TW, v = e % TW;
-      int lv = 1, hi0 = 0, hi1 = 0, ca = u, cb = v;
-      bool ll = true;
-      for (; lv <= L; ++lv) {
-        const int h0 = TH >> lv, h1 = TW >> lv;
-        if (u < h0 && v < h1) continue;
-        hi0 = u >= h0;
-        hi1 = v >= h1;
-        ca = u - hi0 * h0;
-        cb = v - hi1 * h1;
-        ll = false;
-        break;
-      }
-      int gu, gv;
-      if (ll) {
-        gu = (i0 >> L) + u;
-        gv = (j0 >> L) + v;
-      } else {
-        gu = (hi0 ? (M >> lv) : 0) + (i0 >> lv) + ca;
-        gv = (hi1 ? (N >> lv) : 0) + (j0 >> lv) + cb;
-      }
-      const size_t gi = boff + (size_t)gu * N + gv;
-      const float2 w = wa[u][v], bo = __ldcg(a.bw + gi);
+      const size_t gi = mallat_gi(u, v);
+      const float2 w = wa[u][v], bo = wv[u][v];
       const float2 z = make_float2(w.x + bo.x, w.y + bo.y);
       const float2 d = shrinkc(z, tg);
       const float2 bn = make_float2(z.x - d.x, z.y - d.y);

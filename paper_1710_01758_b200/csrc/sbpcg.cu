@@ -1992,7 +1992,7 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
     CK(cudaMemcpy(hst, c->kstamp, sizeof(hst), cudaMemcpyDeviceToHost));
     if (env_flag("SBPCG_KR_PROF", false)) {  // loop segment profile (stderr)
       fprintf(stderr, "KR segments (ns, all iterations):");
-      for (int k = 0; k < 10; ++k) fprintf(stderr, " s%d=%.0f", k, hst[3] ? (double)hst[8 + k] * hst[4] / hst[3] : 0.0);
+      for (int k = 0; k < 19; ++k) fprintf(stderr, " s%d=%.0f", k, hst[3] ? (double)hst[8 + k] * hst[4] / hst[3] : 0.0);
       fprintf(stderr, "\n");
     }
     const double s_per_cyc = hst[3] > 0 ? 1e-9 * (double)hst[4] / (double)hst[3] : 0.0;
