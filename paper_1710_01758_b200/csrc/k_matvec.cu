@@ -275,15 +275,30 @@ __global__ void __launch_bounds__(Split<M>::N2* W)
           a.bout[gi] = bb;
         }
         const float2 r = make_float2(bb.x - (a.mu * av.x + reg.x), bb.y - (a.mu * av.y + reg.y));
-        a.out[gi] = r;
+        if (a.spec) accb[row * W + cc] = r;  // (G = 1) this thread's own accumulator cell
+        else a.out[gi] = r;
         d0 += (double)bb.x * bb.x + (double)bb.y * bb.y;
         d1 += (double)r.x * r.x + (double)r.y * r.y;
       } else {
         const float2 q = make_float2(a.mu * av.x + reg.x, a.mu * av.y + reg.y);
-        a.out[gi] = q;
+        if (MODE != K1_APPLY && a.spec) accb[row * W + cc] = q;
+        else a.out[gi] = q;
         d0 += (double)p.x * q.x + (double)p.y * q.y;
       }
     }
+  }
+  if (MODE != K1_APPLY && a.spec) {
+    // spectral-residual preconditioner: the column spectrum
+    // F_0 q (PCG) or F_0 r0 (RESID) of this tile, from the cells written above (G = 1: the
+    // CTA holds every row of its columns), to `out` in spectral row order
+    __syncthreads();
+    float2 v[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) v[n1] = accb[natidx<M>(j, n1) * W + l];
+    if constexpr (TWR) fft_fwd_r<M, Lay>(v, xch, twr, j, l);
+    else fft_fwd<M, Lay>(v, xch, tw, j, l);
+#pragma unroll
+    for (int s = 0; s < N1; ++s) a.out[boff + (size_t)specidx<M>(j, s) * N + col0 + l] = v[s];
   }
   if constexpr (MODE == K1_APPLY) {
     if (G > 1) cluster.sync();  // peers finished reading this CTA's accb

@@ -72,6 +72,9 @@ __global__ void __launch_bounds__(ColCfg<M, W_>::NT, (ColMinBlocks<M, ColCfg<M, 
   pdl_trigger();
   pdl_wait();
 
+  if constexpr (KIND == P_PRE_C_SPEC) {
+    if (!slice_active(a, b)) return;
+  }
   if constexpr (KIND == P_PRE_A_FWD_COL || KIND == P_PRE_C_INV_COL) {
     if (!slice_active(a, b)) {
       if constexpr (KIND == P_PRE_C_INV_COL) {
@@ -150,6 +153,12 @@ __global__ void __launch_bounds__(ColCfg<M, W_>::NT, (ColMinBlocks<M, ColCfg<M, 
         }
       }
     }
+  } else if constexpr (KIND == P_PRE_C_SPEC) {
+#pragma unroll
+    for (int s = 0; s < N1; ++s) v[s] = a.tmp[boff + (size_t)specidx<M>(j, s) * N + col];
+    fft_inv<M, typename C::Lay>(v, xch, tw, j, l);
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) a.o0[boff + (size_t)natidx<M>(j, n1) * N + col] = v[n1];
   } else if constexpr (KIND == P_ENC_COL) {
     const float2* sc = a.sens + ((size_t)b * a.C + c) * img;
 #pragma unroll
@@ -234,6 +243,12 @@ __global__ void __launch_bounds__(RowCfg<N, LINES_>::NT) k_row(const PassArgs a)
   if constexpr (KIND == P_PRE_B_ROW) {
     b = blockIdx.y;
     if (!slice_active(a, b)) return;
+  } else if constexpr (KIND == P_PRE_B_SPEC) {
+    b = blockIdx.y;
+    if (!slice_active(a, b)) {  // frozen problem: counted once for the graph condition
+      if (a.mode >= 0 && blockIdx.x == 0 && tid == 0) slice_arrive(a.L);
+      return;
+    }
   } else {
     b = blockIdx.y / a.C;
     c = blockIdx.y % a.C;
@@ -259,6 +274,70 @@ __global__ void __launch_bounds__(RowCfg<N, LINES_>::NT) k_row(const PassArgs a)
     if (in_range) {
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) t[natidx<N>(j, n1)] = v[n1];
+    }
+  } else if constexpr (KIND == P_PRE_B_SPEC) {
+    // row rr of the column spectrum: S_r -= alpha Q (PCG iteration), ||r||^2 and <r, z> from
+    // the spectra (Parseval along d0: ||r||^2 = sum |F_0 r|^2 / M; <r, F_0^H T> = <F_0 r, T>)
+    __shared__ double red[32];
+    __shared__ int lastflag;
+    const size_t ro = (size_t)b * img + (size_t)rr * N;
+    const float* li = a.lam_inv + (size_t)b * a.lam_bstride + (size_t)rr * N;
+    float2 sr[N1];
+    float lv[N1];
+    const double alpha = (a.mode == 1) ? a.L.scal[b].alpha : 0.0;
+    {
+      float2 qv[N1];
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) {
+        sr[n1] = a.a0[ro + natidx<N>(j, n1)];
+        qv[n1] = (a.mode == 1) ? a.a1[ro + natidx<N>(j, n1)] : make_float2(0.f, 0.f);
+        lv[n1] = li[specidx<N>(j, n1)];
+      }
+      if (a.mode == 1) {
+#pragma unroll
+        for (int n1 = 0; n1 < N1; ++n1) {
+          sr[n1].x -= (float)alpha * qv[n1].x;
+          sr[n1].y -= (float)alpha * qv[n1].y;
+          if (in_range) a.o0[ro + natidx<N>(j, n1)] = sr[n1];
+        }
+      }
+    }
+    double drr = 0.0, drz = 0.0;
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      v[n1] = sr[n1];
+      if (in_range) drr += (double)sr[n1].x * sr[n1].x + (double)sr[n1].y * sr[n1].y;
+    }
+    fft_fwd<N, typename R::Lay>(v, xch, tw, j, line);
+#pragma unroll
+    for (int s = 0; s < N1; ++s) v[s] = cscale(v[s], lv[s]);
+    fft_inv<N, typename R::Lay>(v, xch, tw, j, line);
+    if (in_range) {
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) {
+        a.tmp[ro + natidx<N>(j, n1)] = v[n1];
+        drz += (double)sr[n1].x * v[n1].x + (double)sr[n1].y * v[n1].y;
+      }
+    }
+    if (a.mode < 0) return;
+    const double s0 = block_sum(drr, red);
+    const double s1 = block_sum(drz, red);
+    const int nblk = gridDim.x;
+    if (publish_and_check_last(s0, s1, a.P, b, blockIdx.x, nblk, &lastflag)) {
+      if (tid < 32) {
+        const double trr = warp_sum_partials(a.P.p0 + (size_t)b * a.P.cap, nblk);
+        const double trz = warp_sum_partials(a.P.p1 + (size_t)b * a.P.cap, nblk);
+        if (tid == 0) {
+          if (a.mode == 1) {
+            fin_rr(a.L, b, trr / (double)M);
+            if (a.L.scal[b].active) fin_rho(a.L, b, trz, false);
+          } else {
+            fin_rho(a.L, b, trz, true);
+          }
+          a.P.cnt[b] = 0;
+          slice_arrive(a.L);
+        }
+      }
     }
   } else if constexpr (KIND == P_ENC_ROW) {
     const float2* t = a.tmp + ((size_t)b * a.C + c) * img + (size_t)rr * N;
@@ -470,7 +549,7 @@ static cudaError_t launch_col_t(const PassArgs& a, cudaStream_t st) {
 }
 template <int N, int KIND>
 static cudaError_t launch_row_t(const PassArgs& a, cudaStream_t st) {
-  const int nimg = (KIND == P_PRE_B_ROW) ? a.B : a.B * a.C;
+  const int nimg = (KIND == P_PRE_B_ROW || KIND == P_PRE_B_SPEC) ? a.B : a.B * a.C;
   constexpr int LBIG = (256 / Split<N>::N2) > 0 ? 256 / Split<N>::N2 : 1;
   constexpr int LSMALL = (32 / Split<N>::N2) > 0 ? 32 / Split<N>::N2 : 1;
   if (((a.M + LBIG - 1) / LBIG) * nimg < kFill) {
@@ -518,6 +597,8 @@ cudaError_t launch_pass(int kind, const PassArgs& a, cudaStream_t st) {
     case P_PRE_A_FWD_COL: return col_dispatch<P_PRE_A_FWD_COL>(a, st);
     case P_PRE_B_ROW: return row_dispatch<P_PRE_B_ROW>(a, st);
     case P_PRE_C_INV_COL: return col_dispatch<P_PRE_C_INV_COL>(a, st);
+    case P_PRE_B_SPEC: return row_dispatch<P_PRE_B_SPEC>(a, st);
+    case P_PRE_C_SPEC: return col_dispatch<P_PRE_C_SPEC>(a, st);
     case P_ENC_COL: return col_dispatch<P_ENC_COL>(a, st);
     case P_ENC_ROW: return row_dispatch<P_ENC_ROW>(a, st);
     case P_ADJ_ROW: return row_dispatch<P_ADJ_ROW>(a, st);

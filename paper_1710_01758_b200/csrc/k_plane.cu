@@ -72,6 +72,11 @@ struct PlaneCfg {
   static constexpr size_t smem = smem0 + (PREF ? sbytes : 0);
 };
 
+// bulk L2 prefetch (TMA engine) of `bytes` (multiple of 16) at a 16-byte aligned global address
+__device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -284,6 +289,20 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
     cp_async_commit();
   };
   if constexpr (PF) prefetch_s(0);
+  // without the shared-memory prefetch buffer: the next coil's s_c rows of this CTA are pulled
+  // into L2 by the bulk-copy engine while this coil is transformed, so the loads that start the
+  // next coil's row stage hit L2 instead of HBM (one elected thread, one 16-byte-multiple row
+  // each; NZ * 8 bytes per row)
+  constexpr bool L2PF = !PF && (MATVEC || MODE == KP_ENCODE) && (NZ * 8) % 16 == 0;
+  auto l2_prefetch_s = [&](int cc) {
+    if (tid < NYL) {
+      const size_t so = ((size_t)b * a.C + cc) * img + (size_t)xpl * PN;
+      l2_prefetch(a.sens + so + (size_t)(G * tid + g) * NZ, (uint32_t)(NZ * sizeof(float2)));
+    }
+  };
+  if constexpr (L2PF) {
+    l2_prefetch_s(0);
+  }
 
   for (int c = 0; c < ncoil; ++c) {
     const size_t soff = ((size_t)b * a.C + c) * img + (size_t)xpl * PN;
@@ -310,6 +329,9 @@ __global__ void __launch_bounds__(PlaneCfg<NY, NZ, G>::T, PlaneCfg<NY, NZ, G>::T
       fft_fwd_t<NZ, typename P::RLay>(v, wb, twz, j, r);
       if constexpr (PF) {  // every thread read sbuf before the barrier inside fft_fwd
         if (c + 1 < ncoil) prefetch_s(c + 1);
+      }
+      if constexpr (L2PF) {
+        if (c + 1 < ncoil) l2_prefetch_s(c + 1);
       }
       __syncthreads();
 #pragma unroll

@@ -30,6 +30,7 @@ struct K1Args {
   int update_u;
   float eps;
   int maxit;
+  int spec;                // 1: write the column spectrum F_0 q (PCG) / F_0 r0 (RESID) instead (G = 1)
   // bookkeeping
   Loop L;
   Partials P;
@@ -269,6 +270,11 @@ enum PassKind {
   P_FIXUP = 10,          // x += alpha p (pending) / x = 0
   P_COL_FWD = 11,        // o0[b][c] = colFFT(a0[b][c]) * scale   (3D: the d0 transform of E)
   P_COL_INV = 12,        // o0[b][c] = colIFFT(a0[b][c]) * scale  (3D: the d0 transform of E^H)
+  // spectral-residual preconditioner (2D line masks, circulant M):
+  // K1 writes the column spectrum Q = F_0 q (RESID: S_r = F_0 r0), so one pass per direction:
+  P_PRE_B_SPEC = 13,     // row k: S_r -= alpha Q (mode 1); T = F_1^H Lambda^-1 F_1 S_r -> tmp;
+                         // ||r||^2 = sum|S_r|^2 / M and <r, z> = Re sum conj(S_r) T (fin_rr, fin_rho)
+  P_PRE_C_SPEC = 14,     // z = F_0^H T (column IFFT), no reductions
 };
 cudaError_t launch_pass(int kind, const PassArgs& a, cudaStream_t st);
 // jinv[b][i] = 1 / (mu f_b sum_c |s_c(i)|^2 + 2 nd lambda + gamma)

@@ -91,6 +91,8 @@ struct sb_ctx {
   int ndim = 2, D0 = 0, D1 = 0, D2 = 1;
   bool plane = false;           // K1P plane kernels (2D non-separable masks, or 3D)
   bool pre2d = false;           // 2D preconditioner as one K1P cluster kernel (KP_PRE2D)
+  bool spec_ok = false;         // spectral-residual preconditioner passes possible (2D lines, G = 1)
+  bool spec_on = false;         // ... and selected for the solve being built / run (circulant M)
   uint8_t* pmask = nullptr;     // 3D: the plane mask [Bm][D1*D2] (mask constant along d0)
   float2 *tw_y = nullptr, *tw_z = nullptr;  // plane twiddles (3D: D1, D2)
   double2 *twd_y = nullptr, *twd_z = nullptr;
@@ -512,6 +514,7 @@ static sb_status seq_resid(sb_ctx* c, Loop L, const float2* bgiven, bool recon, 
   a.eps = eps;
   a.maxit = maxit;
   a.L = L;
+  a.spec = c->spec_on ? 1 : 0;  // r0 leaves as its column spectrum S_r = F_0 r0
   return run_k1(c, K1_RESID, a, st);
 }
 
@@ -530,6 +533,18 @@ static sb_status seq_precond(sb_ctx* c, Loop L, int precond, int mode, const flo
     pa.o1 = c->z;
     pa.jinv = precond == 2 ? c->jinv : nullptr;
     return run_pass(c, P_NOPRE, pa, st);
+  }
+  if (c->spec_on && mode >= 0) {
+    // spectral residual: K1 left S_r = F_0 r0 (RESID) / Q = F_0 q (PCG) in r / q;
+    // one row pass (S_r -= alpha Q, F_1^H Lambda^{-1} F_1, ||r||^2 and <r, z> from the spectra)
+    // and one column pass (z = F_0^H T)
+    pa.a0 = c->r;
+    pa.a1 = c->q;
+    pa.o0 = c->r;
+    pa.tmp = c->tmp;
+    if ((s = run_pass(c, P_PRE_B_SPEC, pa, st))) return s;
+    pa.o0 = zout;
+    return run_pass(c, P_PRE_C_SPEC, pa, st);
   }
   if (c->pre2d) {  // one cluster kernel: r -= alpha q, ||r||^2, z = F^H Lambda^{-1} F r, <r, z>
     KPArgs k = base_kp(c);
@@ -578,6 +593,7 @@ static sb_status seq_body(sb_ctx* c, Loop L, int precond, cudaStream_t st, int* 
   a.x = c->x;
   a.out = c->q;
   a.L = L;
+  a.spec = c->spec_on ? 1 : 0;  // q leaves as its column spectrum Q = F_0 q
   if ((s = run_k1(c, K1_PCG, a, st))) return s;
   if ((s = seq_precond(c, L, precond, 1, c->r, c->z, st))) return s;
   if (nk) *nk = (int)c->launches - n0;
@@ -943,6 +959,7 @@ static sb_status coil_graph_solve(sb_ctx* c, int kind, const sb_pcg_opts* o, con
 }
 
 static sb_status run_solve_kind(sb_ctx* c, int kind, const sb_pcg_opts* o, const float2* ydev) {
+  c->spec_on = c->spec_ok && o->precond == 1;
   if (c->comm && o->use_graph && !c->timing && !c->stage_timing) return coil_graph_solve(c, kind, o, ydev);
   // coil-sharded mode runs the host-driven loop; stage timers need the eager sequence
   if (o->use_graph && !c->timing && !c->comm && !c->stage_timing) {
@@ -1495,6 +1512,9 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
     const int g = atoi(ge);
     if (g >= 1 && g <= 16) c->G = g;  // G need not divide M (uneven rows); g > C leaves idle CTAs
   }
+  // spectral-residual preconditioner passes: 2D line masks whose K1 CTAs hold whole columns
+  // (G = 1) and that do not take the fused one-cluster preconditioner (SBPCG_SPEC=0 disables)
+  c->spec_ok = !d3 && c->separable && c->G == 1 && !c->pre2d && env_flag("SBPCG_SPEC", true);
   // algorithmic bytes per problem-launch of the matvec: coil maps
   // 8NC + z, p_{k-1}, x read + p_k, x, q written (6 x 8N) + the mask (4M floats for line
   // masks, one byte per plane pixel otherwise)

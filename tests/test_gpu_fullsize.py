@@ -161,3 +161,40 @@ def test_config5_launch_shape_fixed_count_sb(c5_small_coils):
                          prm.wavelet_levels, 0.0, 5, "circulant")
     assert relerr(_np(xg)[0], ref) <= 1e-3, relerr(_np(xg)[0], ref)
     ctx.close()
+
+
+@pytest.mark.parametrize("spec", ["1", "0"], ids=["spectral", "three-pass"])
+def test_spectral_residual_preconditioner_batch(monkeypatch, spec):
+    # the spectral-residual preconditioner passes (K1 writes F_0 q / F_0 r0; one row pass with
+    # the S_r update and both dot products; one column pass) on a batch whose K1 CTAs hold whole
+    # columns (G = 1); the fused one-cluster preconditioner is switched off so the batch takes
+    # the pass sequence.  Against the oracle, and against the three-pass preconditioner.
+    monkeypatch.setenv("SBPCG_PRE2D", "0")
+    monkeypatch.setenv("SBPCG_SPEC", spec)
+    from tests.helpers import batch
+    ps = batch(1, 20, (64, 64), 4, amp=100.0)
+    mu, lam, gam = 1.0, 0.05, 0.05
+    sens = np.stack([p["sens"] for p in ps])
+    masks = np.stack([p["mask"] for p in ps])
+    ctx = SbPcg(_t(sens), torch.from_numpy(masks).to(DEV), mu, lam, gam, 1, persistent=False)
+    rng = np.random.default_rng(33)
+    bvec = np.stack([_crandn(rng, 64, 64) for _ in ps])
+    x0 = np.zeros_like(bvec)
+    x, st = ctx.solve(_t(bvec), _t(x0), eps=0.0, max_iters=12, history=True)
+    xt, stt = ctx.solve(_t(bvec), _t(x0), eps=1e-5, max_iters=100)
+    y = np.stack([p["y"] for p in ps])
+    xr, log = ctx.recon(_t(y), 3, eps=0.0, max_iters=8)
+    for bi in (0, 13):
+        p = ps[bi]
+        s32 = _c32(p["sens"])
+        k = precond.build_k(s32, p["mask"], mu, lam, gam)
+        A = lambda v: ops.apply_A(v, s32, p["mask"], mu, lam, gam)  # noqa: E731
+        Mi = lambda v: precond.apply_Minv(v, k)  # noqa: E731
+        ref = pcg(A, _c32(bvec[bi]), x0[bi], Mi, 0.0, 12)
+        assert relerr(_np(x)[bi], ref.x) <= 1e-3
+        np.testing.assert_allclose(st["relres_hist"][bi][:13], ref.relres, rtol=2e-2, atol=1e-6)
+        reft = pcg(A, _c32(bvec[bi]), x0[bi], Mi, 1e-5, 100)
+        assert abs(stt["iters"][bi] - reft.iters) <= 1 and relerr(_np(xt)[bi], reft.x) <= 1e-3
+        refr, _ = sb.sb_recon(_c32(p["y"]), s32, p["mask"], mu, lam, gam, 3, 1, 1, 0.0, 8, "circulant")
+        assert relerr(_np(xr)[bi], refr) <= 1e-3
+    ctx.close()
