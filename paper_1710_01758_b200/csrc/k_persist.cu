@@ -272,9 +272,14 @@ __device__ __forceinline__ void kr_row_pass(const KrArgs& a, KrSmem<M>& S, float
 // data term for the own column vin (shared memory): S.qs = sum_c conj(s_c) F0^H R F0 (s_c vin)
 template <int M, bool SMC>
 __device__ __forceinline__ void kr_dataterm(KrSmem<M>& S, const float2* vin, const float2* coils, const float2* sTb,
-                                            int C, float2* xl, const float2 (&twr)[KrCfg<M>::N1]) {
+                                            int C, float2* xl, const float2 (&twr)[KrCfg<M>::N1], uint32_t mbits,
+                                            float minv) {
+  // shared-memory bandwidth bounds this phase (12 coil lines x ~100 8-byte accesses per lane):
+  // the mask is a bit per spectral slot in a register (mbits; r/M = minv where set), and the coil
+  // sum first adds the lines of a warp with shuffles
   using Cf = KrCfg<M>;
   constexpr int N1 = Cf::N1, N2 = Cf::N2, NT = Cf::NT, LPAR = Cf::LPAR, N = M;
+  constexpr int LW = 32 / N2, NW = NT / 32;  // lines per warp, warps
   const int tid = threadIdx.x, line = tid / N2, j = tid % N2;
   float2 acc[N1];
 #pragma unroll
@@ -289,22 +294,34 @@ __device__ __forceinline__ void kr_dataterm(KrSmem<M>& S, const float2* vin, con
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) v[n1] = cmul(v[n1], vin[N2 * n1 + j]);
     kr_fwd<M>(v, xl, twr, j);
+    const uint32_t mb = act ? mbits : 0u;
 #pragma unroll
-    for (int q = 0; q < N1; ++q) v[q] = cscale(v[q], act ? S.rm[specidx<M>(j, q)] : 0.f);
+    for (int q = 0; q < N1; ++q) v[q] = cscale(v[q], ((mb >> q) & 1u) ? minv : 0.f);
     kr_inv<M>(v, xl, twr, j);
     // acc += conj(s_c) v: the coil line is re-read instead of held in registers
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) acc[n1] = cfmac(SMC ? sc[N2 * n1] : __ldg(sc + N2 * n1), v[n1], acc[n1]);
   }
+  // lines of one warp: fixed shuffle tree (line l + line l + LW/2, ...) -> lanes of line 0
+#pragma unroll
+  for (int off = N2 * LW / 2; off >= N2; off >>= 1)
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      acc[n1].x += __shfl_xor_sync(0xffffffffu, acc[n1].x, off);
+      acc[n1].y += __shfl_xor_sync(0xffffffffu, acc[n1].y, off);
+    }
   __syncthreads();  // exchange areas -> coil-sum buffer
   float2* cs = S.u.xch;
+  const int wid = tid >> 5;
+  if ((tid & 31) < N2) {
 #pragma unroll
-  for (int n1 = 0; n1 < N1; ++n1) cs[line * M + N2 * n1 + j] = acc[n1];
+    for (int n1 = 0; n1 < N1; ++n1) cs[wid * M + N2 * n1 + j] = acc[n1];
+  }
   __syncthreads();
-  const int nl = C < LPAR ? C : LPAR;
-  for (int i = tid; i < M; i += NT) {  // fixed order over the lines
+  const int nw = (C < LPAR ? (C + LW - 1) / LW : NW);
+  for (int i = tid; i < M; i += NT) {  // fixed order over the warps
     float2 sum = cs[i];
-    for (int l = 1; l < nl; ++l) sum = cadd(sum, cs[l * M + i]);
+    for (int w = 1; w < nw; ++w) sum = cadd(sum, cs[w * M + i]);
     S.qs[i] = sum;
   }
   __syncthreads();
@@ -416,6 +433,13 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
   __syncthreads();
   float2 twr[N1];
   load_twr<M>(twr, S.tw, j);
+  // the row mask at this lane's spectral slots as bits (r/M is either 0 or 1/M)
+  // (the host stores r/M = 1.0f / M for sampled rows, sbpcg.cu)
+  uint32_t mbits = 0;
+#pragma unroll
+  for (int q = 0; q < N1; ++q)
+    if (S.rm[specidx<M>(j, q)] != 0.f) mbits |= 1u << q;
+  const float minv = 1.0f / (float)M;
 
   double* part = a.part + (size_t)b * 8 * P;  // 6 slots used (Chronopoulos-Gear phase C)
   float2* xl = S.u.xch + line * XL;
@@ -500,7 +524,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
     }
     __syncthreads();
     seg(10);
-    kr_dataterm<M, SMC>(S, S.pc[1], coils, sTb, C, xl, twr);
+    kr_dataterm<M, SMC>(S, S.pc[1], coils, sTb, C, xl, twr, mbits, minv);
     seg(11);
     double d0 = 0.0, d1 = 0.0;
     for (int i = tid; i < M; i += NT) {
@@ -584,7 +608,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
         double rz = kr_col_inv_z<M>(S, a.Tb, xl, twr, boff, t);
         __syncthreads();
         seg(0);
-        kr_dataterm<M, SMC>(S, S.zc[1], coils, sTb, C, xl, twr);
+        kr_dataterm<M, SMC>(S, S.zc[1], coils, sTb, C, xl, twr, mbits, minv);
         seg(1);
         double dd = 0.0, drr = 0.0, de = 0.0, dq = 0.0, dp = 0.0;
         for (int i = tid; i < M; i += NT) {
@@ -772,7 +796,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
       }
       __syncthreads();
       seg(0);
-      kr_dataterm<M, SMC>(S, S.pc[1], coils, sTb, C, xl, twr);
+      kr_dataterm<M, SMC>(S, S.pc[1], coils, sTb, C, xl, twr, mbits, minv);
       seg(1);
       double ds = 0.0, dz = 0.0;
       for (int i = tid; i < M; i += NT) {
