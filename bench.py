@@ -168,6 +168,18 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def load_pipes(cfg):
+    """FP32-issue co-limit of the dominant kernel: FMA-pipe busy %, issue-active %,
+    warps-active % from the last ncu metric pass (tools/gpu_pipes.sh -> profiles/ncu_pipes.json)."""
+    path = os.path.join(ROOT, "profiles", "ncu_pipes.json")
+    if os.path.exists(path):
+        d = json.load(open(path)).get(f"config{cfg}")
+        if d:
+            return {k: d[k] for k in ("kernel", "fma_pipe_busy_pct", "issue_active_pct", "warps_active_pct",
+                                      "fma_inst_share", "source")}
+    return None
+
+
 def load_traffic(cfg):
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(path):
@@ -507,7 +519,8 @@ def bench_config(cfg, args, ws, rank, dist, dev, main):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s", "frac": achieved / pk,
                 "traffic": load_traffic(cfg) if which == 0 else load_traffic(f"{cfg}_kr"),
                 "peak_kind": peak_kind, "kernel": kname, "kernel_avg_us": k_avg_s * 1e6,
-                "kernel_launches_timed": k_n, "alg_bytes_per_launch": k_bytes}
+                "kernel_launches_timed": k_n, "alg_bytes_per_launch": k_bytes,
+                "fp32_colimit": load_pipes(cfg)}
 
     res = {"value": value, "ms_per_step": t_max / steps, "steps": steps, "warmup": warmup,
            "problems_per_gpu": per, "pcg_iters_per_step": it_sum / steps / (1 if coil_mode else ws),
