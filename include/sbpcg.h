@@ -275,6 +275,20 @@ sb_status sb_normalize_coil_images(const sb_c64* m, const sb_c64* sens_hat, int3
 sb_status sb_coil_compress(const sb_c64* y, const sb_c64* sens, int32_t batch, int32_t coils, int64_t npix,
                            int32_t coils_out, sb_c64* y_out, sb_c64* sens_out, float* eig_out, void* stream);
 
+/* Readout decoupling (BASELINE config 4; "fully sampled" readout):
+ * for a 3D acquisition whose mask is constant along the readout d0, F_3 = F_0 (x) F_12 and
+ * R = I_0 (x) R_12, so the unitary 1D IFFT along d0 of every coil's k-space splits the problem
+ * into D0 independent 2D problems on the (d1, d2) planes:
+ *   y2[x][c][k1][k2] = (F_0^H y3[c])(x, k1, k2),   s2[x][c][d1][d2] = s3[c][x][d1][d2]
+ * (the maps are image-space: only their layout changes; the plane mask is the 3D mask's
+ * d0 = 0 plane).  The y2 / s2 stacks are the [B][C][d1][d2] inputs of a 2D context with
+ * B = D0 problems and mask_shared = 1.  shape = {D0, D1, D2}; D0 in the column-FFT size set
+ * (8..256, 192); D1 * D2 a multiple of 8.  y3, s3: complex [C][D0][D1][D2]; y2, s2: complex
+ * [D0][C][D1][D2]; s3 = s2 = NULL skips the maps.  DEVICE pointers only (SB_E_ARG otherwise);
+ * outputs must not alias inputs.  Synchronous on `stream`. */
+sb_status sb_readout_decouple(const sb_c64* y3, const sb_c64* s3, int32_t coils, const int64_t* shape, sb_c64* y2,
+                              sb_c64* s2, void* stream);
+
 /* Number of kernels launched by this context since creation (for bench.py). */
 int64_t sb_kernel_launch_count(const sb_ctx* ctx);
 

@@ -6,7 +6,7 @@ be imported (and run) before the library exists; any use of the compute path wit
 built library raises ImportError (there is no CPU fallback)."""
 
 _EXPORTS = ("SbPcg", "SbError", "SbComm", "coil_shard", "normalize_sens", "normalize_coil_images",
-            "coil_compress", "abi_version", "LIB_PATH")
+            "coil_compress", "readout_decouple", "abi_version", "LIB_PATH")
 
 
 def __getattr__(name):

@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(ColCfg<M, W_>::NT, (ColMinBlocks<M, ColCfg<M, 
 
   // image / problem index
   int b, c = 0;
-  if constexpr (KIND == P_ENC_COL || KIND == P_COL_FWD || KIND == P_COL_INV) {
+  if constexpr (KIND == P_ENC_COL || KIND == P_COL_FWD || KIND == P_COL_INV || KIND == P_COL_DECOUPLE) {
     b = blockIdx.y / a.C;
     c = blockIdx.y % a.C;
   } else {
@@ -187,6 +187,15 @@ __global__ void __launch_bounds__(ColCfg<M, W_>::NT, (ColMinBlocks<M, ColCfg<M, 
       for (int n1 = 0; n1 < N1; ++n1)
         a.o0[ioff + (size_t)natidx<M>(j, n1) * N + col] = make_float2(v[n1].x * a.scale, v[n1].y * a.scale);
     }
+  } else if constexpr (KIND == P_COL_DECOUPLE) {
+    // readout decoupling: the unitary 1D IFFT along the fully sampled readout
+    // d0 of coil c's k-space, written plane-major: o0[x][c][k12]
+#pragma unroll
+    for (int s = 0; s < N1; ++s) v[s] = a.a0[(size_t)c * img + (size_t)specidx<M>(j, s) * N + col];
+    fft_inv<M, typename C::Lay>(v, xch, tw, j, l);
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1)
+      a.o0[((size_t)natidx<M>(j, n1) * a.C + c) * N + col] = make_float2(v[n1].x * a.scale, v[n1].y * a.scale);
   } else if constexpr (KIND == P_ADJ_COL) {
     float2 acc[N1];
     float rss[N1];
@@ -532,7 +541,7 @@ constexpr int kFill = 2 * 148;
 
 template <int M, int KIND>
 static cudaError_t launch_col_t(const PassArgs& a, cudaStream_t st) {
-  const int nimg = (KIND == P_ENC_COL || KIND == P_COL_FWD || KIND == P_COL_INV) ? a.B * a.C : a.B;
+  const int nimg = (KIND == P_ENC_COL || KIND == P_COL_FWD || KIND == P_COL_INV || KIND == P_COL_DECOUPLE) ? a.B * a.C : a.B;
   constexpr int WS = (32 / Split<M>::N2) > 2 ? 32 / Split<M>::N2 : 2;  // >= one warp per CTA
   if (WS < 8 && (a.N / 8) * nimg < kFill) {
     return launch_ex(k_col<M, (WS < 8 ? WS : 8), KIND>, dim3(a.N / WS, nimg), dim3(ColCfg<M, (WS < 8 ? WS : 8)>::NT),
@@ -599,6 +608,7 @@ cudaError_t launch_pass(int kind, const PassArgs& a, cudaStream_t st) {
     case P_PRE_C_INV_COL: return col_dispatch<P_PRE_C_INV_COL>(a, st);
     case P_PRE_B_SPEC: return row_dispatch<P_PRE_B_SPEC>(a, st);
     case P_PRE_C_SPEC: return col_dispatch<P_PRE_C_SPEC>(a, st);
+    case P_COL_DECOUPLE: return col_dispatch<P_COL_DECOUPLE>(a, st);
     case P_ENC_COL: return col_dispatch<P_ENC_COL>(a, st);
     case P_ENC_ROW: return row_dispatch<P_ENC_ROW>(a, st);
     case P_ADJ_ROW: return row_dispatch<P_ADJ_ROW>(a, st);

@@ -275,6 +275,7 @@ enum PassKind {
   P_PRE_B_SPEC = 13,     // row k: S_r -= alpha Q (mode 1); T = F_1^H Lambda^-1 F_1 S_r -> tmp;
                          // ||r||^2 = sum|S_r|^2 / M and <r, z> = Re sum conj(S_r) T (fin_rr, fin_rho)
   P_PRE_C_SPEC = 14,     // z = F_0^H T (column IFFT), no reductions
+  P_COL_DECOUPLE = 15,   // readout decoupling: o0[x][c] = colIFFT(a0[c])[x] * scale (B = 1)
 };
 cudaError_t launch_pass(int kind, const PassArgs& a, cudaStream_t st);
 // jinv[b][i] = 1 / (mu f_b sum_c |s_c(i)|^2 + 2 nd lambda + gamma)

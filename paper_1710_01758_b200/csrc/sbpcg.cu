@@ -1719,6 +1719,42 @@ sb_status sb_coil_compress(const sb_c64* y, const sb_c64* sens, int32_t batch, i
   return SB_OK;
 }
 
+sb_status sb_readout_decouple(const sb_c64* y3, const sb_c64* s3, int32_t coils, const int64_t* shape, sb_c64* y2,
+                              sb_c64* s2, void* stream) {
+  if (!y3 || !shape || !y2 || coils < 1 || (s3 == nullptr) != (s2 == nullptr)) return SB_E_ARG;
+  if (!is_device_ptr(y3) || !is_device_ptr(y2) || (s3 && (!is_device_ptr(s3) || !is_device_ptr(s2)))) return SB_E_ARG;
+  const int64_t D0 = shape[0], D1 = shape[1], D2 = shape[2];
+  if (D1 < 1 || D2 < 1 || !col3_len_ok(D0) || (D1 * D2) % 8 != 0 || (int64_t)coils > 65535) return SB_E_UNSUPPORTED_SIZE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t n12 = (size_t)D1 * D2;
+  auto tw = make_tw<float2>((int)D0);
+  float2* twd = nullptr;
+  if (cudaMalloc(&twd, D0 * sizeof(float2)) != cudaSuccess) return SB_E_NOMEM;
+  PassArgs a;
+  memset(&a, 0, sizeof(a));
+  a.B = 1;
+  a.C = coils;
+  a.M = (int)D0;
+  a.N = (int)n12;
+  a.tw_m = twd;
+  a.a0 = (const float2*)y3;
+  a.o0 = (float2*)y2;
+  a.scale = 1.0f / std::sqrt((float)D0);
+  sb_status rs = SB_OK;
+  if (cudaMemcpyAsync(twd, tw.data(), D0 * sizeof(float2), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      launch_pass(P_COL_DECOUPLE, a, st) != cudaSuccess)
+    rs = SB_E_CUDA;
+  // image-space maps change layout only: s2[x][c] = s3[c][x] (one strided 2D copy per coil)
+  for (int c = 0; s3 && rs == SB_OK && c < coils; ++c)
+    if (cudaMemcpy2DAsync((float2*)s2 + (size_t)c * n12, (size_t)coils * n12 * sizeof(float2),
+                          (const float2*)s3 + (size_t)c * D0 * n12, n12 * sizeof(float2), n12 * sizeof(float2),
+                          (size_t)D0, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      rs = SB_E_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) rs = SB_E_CUDA;
+  cudaFree(twd);
+  return rs;
+}
+
 sb_status sb_set_wavelet(sb_ctx* c, int32_t family) {
   sb_status s = check_ready(c);
   if (s) return s;

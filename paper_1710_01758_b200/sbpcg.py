@@ -84,6 +84,7 @@ _sig = {
     "sb_normalize_coil_images": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_int64, _vp, _vp]),
     "sb_coil_compress": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_int64, C.c_int32, _vp, _vp,
                                    C.POINTER(C.c_float), _vp]),
+    "sb_readout_decouple": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(C.c_int64), _vp, _vp, _vp]),
     "sb_pcg_destroy": (None, [_vp]),
     "sb_status_str": (C.c_char_p, [C.c_int]),
     "sb_last_error": (C.c_char_p, [_vp]),
@@ -407,6 +408,26 @@ def coil_compress(y: torch.Tensor, sens: torch.Tensor, coils_out: int):
     if st != 0:
         raise SbError(st, "sb_coil_compress")
     return yo, so, torch.tensor(list(ev), dtype=torch.float32).view(B, Cc)
+
+
+def readout_decouple(y3: torch.Tensor, s3: Optional[torch.Tensor] = None):
+    """Readout decoupling (include/sbpcg.h sb_readout_decouple): y3, s3 complex64 CUDA tensors
+    [C, D0, D1, D2] -> (y2, s2) [D0, C, D1, D2], the batch of D0 independent 2D problems."""
+    if y3.dtype != torch.complex64 or not y3.is_cuda or y3.dim() != 4:
+        raise TypeError("y3 must be a complex64 CUDA tensor [C, D0, D1, D2]")
+    if s3 is not None and (s3.shape != y3.shape or s3.dtype != torch.complex64 or s3.device != y3.device):
+        raise ValueError("s3 must match y3")
+    Cc, D0, D1, D2 = (int(v) for v in y3.shape)
+    y3 = y3.contiguous()
+    s3c = s3.contiguous() if s3 is not None else None  # kept alive across the call
+    y2 = torch.empty((D0, Cc, D1, D2), dtype=torch.complex64, device=y3.device)
+    s2 = torch.empty_like(y2) if s3 is not None else None
+    shp = (C.c_int64 * 3)(D0, D1, D2)
+    st = _lib.sb_readout_decouple(_ptr(y3), _ptr(s3c) if s3c is not None else None, Cc, shp, _ptr(y2),
+                                  _ptr(s2) if s2 is not None else None, _stream())
+    if st != 0:
+        raise SbError(st, "sb_readout_decouple")
+    return y2, s2
 
 
 def coil_shard(coils: int, rank: int, world: int):
