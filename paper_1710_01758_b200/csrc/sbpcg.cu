@@ -1033,7 +1033,19 @@ static sb_status run_kr(sb_ctx* c, int n_outer, const sb_pcg_opts* o, int par0) 
     e0 = ev_get(c);
     CK(cudaEventRecord(e0, c->st));
   }
-  CK(launch_kr(a, c->st));
+  {
+    const cudaError_t e = launch_kr(a, c->st);
+    if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorLaunchOutOfResources) {
+      // the problems do not fit one cooperative launch on this device after all (the limit was
+      // estimated at create): drop the persistent path for this context; the caller re-runs the
+      // call on the kernel sequence (no work of this launch has been enqueued)
+      cudaGetLastError();
+      c->kr_ok = false;
+      c->err = std::string("persistent kernel not launchable, using the kernel sequence: ") + cudaGetErrorString(e);
+      return SB_E_UNSUPPORTED_SIZE;
+    }
+    CK(e);
+  }
   c->launches++;
   if (c->timing) {
     e1 = ev_get(c);
@@ -1944,8 +1956,13 @@ sb_status sb_pcg_solve(sb_ctx* c, const sb_c64* b, sb_c64* x, const sb_pcg_opts*
   CK(cudaMemcpyAsync(c->x, x, bytes, xdev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
   CK(cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st));
   if (c->timing) c->evnext = 0;
-  const bool kr = use_kr(c, o);
-  if ((s = kr ? run_kr(c, 0, o, 0) : run_solve_kind(c, 0, o, nullptr))) return s;
+  bool kr = use_kr(c, o);
+  s = kr ? run_kr(c, 0, o, 0) : run_solve_kind(c, 0, o, nullptr);
+  if (s == SB_E_UNSUPPORTED_SIZE && kr && !c->kr_ok) {  // persistent launch refused: kernel sequence
+    kr = false;
+    s = run_solve_kind(c, 0, o, nullptr);
+  }
+  if (s) return s;
   CK(cudaMemcpyAsync(x, c->x, bytes, xdev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   std::vector<Scal> hs(c->B);
@@ -2006,7 +2023,7 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
   CK(cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st));
   if (c->timing) c->evnext = 0;
   const sb_pcg_opts* o = &ro->pcg;
-  const bool kr = use_kr(c, o);
+  bool kr = use_kr(c, o);
   c->stage_timing = kr ? false : (ro->stage_timers != 0);
   for (double& v : c->stage_s) v = 0.0;
   c->stage_ev.clear();
@@ -2020,8 +2037,15 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
     CK(cudaEventRecord(ei1, c->st));
     c->stage_ev.push_back({ST_INIT, {ei0, ei1}});
     CK(cudaMemsetAsync(c->kstamp, 0, 32 * sizeof(unsigned long long), c->st));
-    if ((s = run_kr(c, ro->n_outer, o, 0))) return s;
-  } else {
+    s = run_kr(c, ro->n_outer, o, 0);
+    if (s == SB_E_UNSUPPORTED_SIZE && !c->kr_ok) {  // persistent launch refused: kernel sequence
+      kr = false;
+      c->stage_timing = ro->stage_timers != 0;
+    } else if (s) {
+      return s;
+    }
+  }
+  if (!kr) {
     if ((s = run_solve_kind(c, 1, o, (const float2*)yd))) return s;
     for (int j = 1; j < ro->n_outer; ++j) {
       const int par = (j - 1) & 1;  // b_x/b_y buffer parity
