@@ -604,6 +604,15 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
       double rho_prev = 0.0;
       for (int kc = 0;; ++kc) {  // kc: index of the z_kc, w_kc formed in this pass
         seg(-1);
+        // skew probe (SBPCG_KR_PROF=2): globaltimer at phase-C start / end / barrier exit of
+        // every CTA of problem 0, pass 4 of the first solve -> stamp[32 + 4 t + {0, 1, 2}]
+        const bool probe = a.prof == 2 && js == 0 && kc == 4 && tid == 0 && b == 0;
+        auto gtime = []() {
+          unsigned long long g;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+          return g;
+        };
+        if (probe) a.stamp[32 + 4 * t] = gtime();
         // ---- z_kc = F0^H T (columns t-1, t, t+1), w = A z, W = F0 w ; rho, delta, ||r||^2
         double rz = kr_col_inv_z<M>(S, a.Tb, xl, twr, boff, t);
         __syncthreads();
@@ -641,7 +650,9 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
           }
         }
         seg(2);
+        if (probe) a.stamp[32 + 4 * t + 1] = gtime();
         pbar(barc, target, P);
+        if (probe) a.stamp[32 + 4 * t + 2] = gtime();
         seg(3);
         // row t of W: its L2 round trip overlaps the all-reduce read (cp.async, no registers)
         for (int e = tid; e < N / 2; e += NT) kr_cp16(S.wrow + 2 * e, a.Qs + boff + (size_t)t * N + 2 * e);

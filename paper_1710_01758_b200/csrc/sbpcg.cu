@@ -1020,7 +1020,7 @@ static sb_status run_kr(sb_ctx* c, int n_outer, const sb_pcg_opts* o, int par0) 
   a.part = c->P.p0;
   a.bar = c->kbar;
   a.stamp = c->kstamp;
-  a.prof = env_flag("SBPCG_KR_PROF", false) ? 1 : 0;
+  a.prof = getenv("SBPCG_KR_PROF") ? atoi(getenv("SBPCG_KR_PROF")) : 0;
   a.cg = c->kr_cg ? 1 : 0;
   a.L = make_loop(c, 0ull);
   a.n_outer = n_outer;
@@ -1544,7 +1544,7 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
   c->kr_ok = !d3 && c->separable && kr_supported(c->M, c->N, c->L) && c->B <= kr_max_problems(c->M, c->N, c->C);
   if (!s && c->kr_ok) {
     if (dalloc(&c->sT, BCN) != cudaSuccess || dalloc(&c->kbar, c->B) != cudaSuccess ||
-        dalloc(&c->kstamp, 32) != cudaSuccess) {
+        dalloc(&c->kstamp, 32 + 4 * 256) != cudaSuccess) {
       cudaGetLastError();
       sb_pcg_destroy(c);
       return SB_E_NOMEM;
@@ -2070,7 +2070,16 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
   if (kr) {  // the kernel's stage cycle counters, converted with its own cycles -> ns ratio
     unsigned long long hst[32];
     CK(cudaMemcpy(hst, c->kstamp, sizeof(hst), cudaMemcpyDeviceToHost));
-    if (env_flag("SBPCG_KR_PROF", false)) {  // loop segment profile (stderr)
+    if (getenv("SBPCG_KR_PROF") && atoi(getenv("SBPCG_KR_PROF")) == 2 && c->N <= 256) {  // skew probe dump
+      std::vector<unsigned long long> pr(4 * 256);
+      CK(cudaMemcpy(pr.data(), c->kstamp + 32, pr.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+      FILE* f = fopen("gpurun_out/kr_skew.txt", "w");
+      if (f) {
+        for (int t = 0; t < c->N; ++t) fprintf(f, "%d %llu %llu %llu\n", t, pr[4 * t], pr[4 * t + 1], pr[4 * t + 2]);
+        fclose(f);
+      }
+    }
+    if (getenv("SBPCG_KR_PROF") && atoi(getenv("SBPCG_KR_PROF")) > 0) {  // loop segment profile (stderr)
       fprintf(stderr, "KR segments (ns, all iterations):");
       for (int k = 0; k < 19; ++k) fprintf(stderr, " s%d=%.0f", k, hst[3] ? (double)hst[8 + k] * hst[4] / hst[3] : 0.0);
       fprintf(stderr, "\n");

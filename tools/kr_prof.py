@@ -3,7 +3,7 @@ ns per iteration of each loop segment as seen by CTA 0 of problem 0."""
 import os
 import sys
 
-os.environ["SBPCG_KR_PROF"] = "1"
+os.environ.setdefault("SBPCG_KR_PROF", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
