@@ -133,11 +133,14 @@ sb_status sb_set_wavelet(sb_ctx* ctx, int32_t family);
 
 /* Replace the coil sensitivities (same shape; host or device pointer, copied) and rebuild
  * Lambda.  The mask, weights, buffers and captured CUDA graphs stay valid,
- * so a new acquisition with the same geometry reuses the context.  Synchronises the stream. */
+ * so a new acquisition with the same geometry reuses the context.  Asynchronous (a host `sens`
+ * must stay valid until the next synchronising call); a singular k of the rebuilt Lambda is
+ * reported as SB_E_SINGULAR_K by the next sb_pcg_solve / sb_recon / sb_pcg_get_k. */
 sb_status sb_pcg_update_sens(sb_ctx* ctx, const sb_c64* sens);
 
 /* Rebuild Lambda^{-1} from the context's sens/mask/weights (the preconditioner build of
- * PAPER.md:238 / Table 2, timed by bench.py as part of a step). */
+ * PAPER.md:238 / Table 2, timed by bench.py as part of a step).  Asynchronous; a singular k
+ * is reported by the next sb_pcg_solve / sb_recon / sb_pcg_get_k (SB_E_SINGULAR_K). */
 sb_status sb_pcg_build_precond(sb_ctx* ctx);
 
 /* y = A x for all B problems.  x, y: complex [B][d0][d1]. */

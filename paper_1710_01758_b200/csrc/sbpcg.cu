@@ -166,6 +166,11 @@ struct sb_ctx {
   std::vector<cudaEvent_t> stage_pool;
   size_t stage_next = 0;
   double build_s = 0;
+  // the Lambda build is asynchronous: its singular-k flag (pinned host copy) and its event pair
+  // are checked by the next call that completes the stream (build_checked)
+  int* bad_host = nullptr;
+  bool build_check = false;
+  cudaEvent_t bev[2] = {nullptr, nullptr};
   // kernel timing (0 = matvec K1/K1P, 1 = unused, 2 = persistent kernel KR)
   bool timing = false;
   double t_ms[3] = {0, 0, 0};
@@ -1092,16 +1097,28 @@ static cudaError_t lscratch(sb_ctx* c, int slot, T** p, size_t n) {
 static sb_status build_lambda_impl(sb_ctx* c);
 // Lambda build timed with an event pair (sb_recon_log.build_s; Table 2 analogue).
 static sb_status build_lambda(sb_ctx* c) {
-  cudaEvent_t e0 = stage_event(c), e1 = stage_event(c);
-  c->stage_next -= 2;  // scratch use: not part of a recon's stage list
-  CK(cudaEventRecord(e0, c->st));
+  if (!c->bev[0]) {
+    CK(cudaEventCreate(&c->bev[0]));
+    CK(cudaEventCreate(&c->bev[1]));
+  }
+  if (!c->bad_host) CK(cudaMallocHost(&c->bad_host, sizeof(int)));
+  CK(cudaEventRecord(c->bev[0], c->st));
   sb_status s = build_lambda_impl(c);
   if (s) return s;
-  CK(cudaEventRecord(e1, c->st));
-  CK(cudaEventSynchronize(e1));
+  CK(cudaEventRecord(c->bev[1], c->st));
+  c->build_check = true;  // no host synchronisation: the next solve / recon overlaps its enqueue
+  return SB_OK;
+}
+
+// After a stream synchronisation: the last Lambda build's time (sb_recon_log.build_s) and its
+// singular-k flag (SB_E_SINGULAR_K is reported by the first synchronising call after the build).
+static sb_status build_checked(sb_ctx* c) {
+  if (!c->build_check) return SB_OK;
+  c->build_check = false;
   float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, e0, e1));
-  c->build_s = 1e-3 * ms;
+  if (cudaEventElapsedTime(&ms, c->bev[0], c->bev[1]) == cudaSuccess) c->build_s = 1e-3 * ms;
+  cudaGetLastError();
+  if (*c->bad_host) return fail(c, SB_E_SINGULAR_K, "singular k (min |k| <= 1e-14 or non-finite)");
   return SB_OK;
 }
 
@@ -1225,11 +1242,8 @@ static sb_status build_lambda3(sb_ctx* c) {
 }
 
 static sb_status finish_lambda(sb_ctx* c, void* tmp, void* g, void* rh, int* bad, void* kc2) {
-  int hb = 0;
-  CK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
+  CK(cudaMemcpyAsync(c->bad_host, bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
   (void)tmp, (void)g, (void)rh, (void)kc2;  // persistent scratch (lscratch)
-  if (hb) return fail(c, SB_E_SINGULAR_K, "singular k (min |k| <= 1e-14 or non-finite)");
   return SB_OK;
 }
 
@@ -1305,6 +1319,9 @@ void sb_pcg_destroy(sb_ctx* c) {
     for (auto& g : row)
       if (g) cudaGraphDestroy(g);
   if (c->cst) cudaStreamDestroy(c->cst);
+  if (c->bad_host) cudaFreeHost(c->bad_host);
+  for (auto e : c->bev)
+    if (e) cudaEventDestroy(e);
   void* bufs[] = {c->sens, c->mask, c->rowmask, c->lam_inv, c->kbuf, c->tw_m, c->tw_n, c->twd_m, c->twd_n,
                   c->x, c->r, c->z, c->q, c->p0, c->p1, c->tmp, c->bvec, c->u, c->u1, c->rhs,
                   c->bx[0], c->bx[1], c->by[0], c->by[1], c->bw, c->tmpc, c->stage_in, c->stage_out,
@@ -1576,6 +1593,7 @@ sb_status sb_pcg_create(sb_ctx** out, const sb_dims* dims, int32_t coils, const 
     if (const char* cu = getenv("SBPCG_COIL_UNROLL")) c->coil_unroll = std::max(1, std::min(16, atoi(cu)));
   }
   s = build_lambda(c);
+  if (!s) s = cudaStreamSynchronize(c->st) == cudaSuccess ? build_checked(c) : SB_E_CUDA;
   if (s) {
     sb_pcg_destroy(c);
     return s;
@@ -1965,6 +1983,7 @@ sb_status sb_pcg_solve(sb_ctx* c, const sb_c64* b, sb_c64* x, const sb_pcg_opts*
   if (s) return s;
   CK(cudaMemcpyAsync(x, c->x, bytes, xdev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+  if ((s = build_checked(c))) return s;
   std::vector<Scal> hs(c->B);
   CK(cudaMemcpy(hs.data(), c->scal, sizeof(Scal) * c->B, cudaMemcpyDeviceToHost));
   if (c->timing) {
@@ -2061,6 +2080,7 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
                      c->st));
   CK(cudaEventRecord(e1, c->st));
   CK(cudaStreamSynchronize(c->st));
+  if ((s = build_checked(c))) return s;
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
@@ -2173,7 +2193,7 @@ sb_status sb_pcg_get_k(sb_ctx* c, double* k_out) {
   CK(cudaMemcpyAsync(k_out, c->kbuf, bytes, is_device_ptr(k_out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                      c->st));
   CK(cudaStreamSynchronize(c->st));
-  return SB_OK;
+  return build_checked(c);
 }
 
 sb_status sb_set_kernel_timing(sb_ctx* c, int32_t enable) {

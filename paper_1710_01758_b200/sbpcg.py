@@ -210,6 +210,7 @@ class SbPcg:
         if tuple(sens.shape) != tuple(self._sens.shape) or sens.dtype != torch.complex64:
             raise ValueError("update_sens: shape/dtype must match the context")
         sens = sens.contiguous()
+        self._sens_upload = sens  # the copy is asynchronous: keep the source alive until the next call
         self._check(_lib.sb_pcg_update_sens(self._h, _ptr(sens)), "update_sens")
 
     def build_precond(self):

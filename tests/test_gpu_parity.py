@@ -313,3 +313,25 @@ def test_update_sens_equals_fresh_context():
 def problems_kspace(p, mask):
     from oracle import problems
     return problems.make_kspace(p["phantom"], p["sens"], mask, p["noise"])
+
+
+def test_singular_k_reporting():
+    # k >= gamma > 0 for finite maps, so only non-finite coil maps make Lambda singular
+    # (SB_E_SINGULAR_K): reported by create (synchronous), and after the asynchronous rebuild of
+    # sb_pcg_update_sens by the next synchronising call (include/sbpcg.h)
+    ps = batch(1, 1, (64, 64), 4)
+    bad = np.stack([ps[0]["sens"]]).copy()
+    bad[0, 1, 5, 7] = np.nan
+    with pytest.raises(SbError) as ei:
+        _ctx([dict(sens=bad[0], mask=ps[0]["mask"])], 1.0, 0.05, 0.05, 1)
+    assert ei.value.status == 5
+    ctx = _ctx(ps, 1.0, 0.05, 0.05, 1)
+    ctx.update_sens(_t(bad))
+    y = _t(ps[0]["y"][None])
+    with pytest.raises(SbError) as ei:
+        ctx.recon(y, 1, eps=0.0, max_iters=2)
+    assert ei.value.status == 5
+    ctx.update_sens(_t(np.stack([ps[0]["sens"]])))  # healthy maps again: the context recovers
+    x, log = ctx.recon(y, 1, eps=0.0, max_iters=2)
+    assert torch.isfinite(x).all()
+    ctx.close()
