@@ -170,6 +170,11 @@ struct sb_ctx {
   // are checked by the next call that completes the stream (build_checked)
   int* bad_host = nullptr;
   bool build_check = false;
+  // pinned host copies of the per-call results (scalars, logs, stage counters), filled by async
+  // copies enqueued before the call's final synchronisation (no blocking copies after it)
+  unsigned char* hres = nullptr;
+  size_t hres_bytes = 0;
+  cudaEvent_t rev[2] = {nullptr, nullptr};  // sb_recon's total_ms event pair
   cudaEvent_t bev[2] = {nullptr, nullptr};
   // kernel timing (0 = matvec K1/K1P, 1 = unused, 2 = persistent kernel KR)
   bool timing = false;
@@ -1264,15 +1269,45 @@ static sb_status check_ready(sb_ctx* c) {
   return SB_OK;
 }
 
-static sb_status status_from_scal(sb_ctx* c) {
-  std::vector<Scal> hs(c->B);
-  CK(cudaMemcpy(hs.data(), c->scal, sizeof(Scal) * c->B, cudaMemcpyDeviceToHost));
+// Pinned results block: [Scal x B][log_iters][log_relres][kstamp x 32][hist]
+struct HostRes {
+  Scal* scal;
+  int32_t* iters;
+  float* relres;
+  unsigned long long* stamp;
+  float* hist;
+};
+static sb_status host_results(sb_ctx* c, int slots, HostRes* h) {
+  const size_t nb = sizeof(Scal) * c->B, nl = (size_t)slots * c->B;
+  const size_t need = nb + nl * 4 * 2 + 32 * 8 + (size_t)c->B * c->hist_stride * 4 + 64;
+  if (c->hres_bytes < need) {
+    if (c->hres) cudaFreeHost(c->hres);
+    c->hres = nullptr;
+    c->hres_bytes = 0;
+    CK(cudaMallocHost(&c->hres, need));
+    c->hres_bytes = need;
+  }
+  unsigned char* q = c->hres;
+  h->scal = reinterpret_cast<Scal*>(q);
+  q += (nb + 15) / 16 * 16;
+  h->iters = reinterpret_cast<int32_t*>(q);
+  q += (nl * 4 + 15) / 16 * 16;
+  h->relres = reinterpret_cast<float*>(q);
+  q += (nl * 4 + 15) / 16 * 16;
+  h->stamp = reinterpret_cast<unsigned long long*>(q);
+  q += 32 * 8;
+  h->hist = reinterpret_cast<float*>(q);
+  return SB_OK;
+}
+
+static sb_status status_of(sb_ctx* c, const Scal* hs) {
   for (int b = 0; b < c->B; ++b) {
     if (hs[b].status == ST_NONFINITE) return fail(c, SB_E_NONFINITE, "non-finite PCG scalar in problem " + std::to_string(b));
     if (hs[b].status == ST_INDEFINITE) return fail(c, SB_E_INDEFINITE, "<p, A p> <= 0 in problem " + std::to_string(b));
   }
   return SB_OK;
 }
+
 
 // ================================================================== C ABI
 extern "C" {
@@ -1320,6 +1355,9 @@ void sb_pcg_destroy(sb_ctx* c) {
       if (g) cudaGraphDestroy(g);
   if (c->cst) cudaStreamDestroy(c->cst);
   if (c->bad_host) cudaFreeHost(c->bad_host);
+  if (c->hres) cudaFreeHost(c->hres);
+  for (auto e : c->rev)
+    if (e) cudaEventDestroy(e);
   for (auto e : c->bev)
     if (e) cudaEventDestroy(e);
   void* bufs[] = {c->sens, c->mask, c->rowmask, c->lam_inv, c->kbuf, c->tw_m, c->tw_n, c->twd_m, c->twd_n,
@@ -1982,10 +2020,15 @@ sb_status sb_pcg_solve(sb_ctx* c, const sb_c64* b, sb_c64* x, const sb_pcg_opts*
   }
   if (s) return s;
   CK(cudaMemcpyAsync(x, c->x, bytes, xdev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
+  HostRes hr;
+  if ((s = host_results(c, 1, &hr))) return s;
+  CK(cudaMemcpyAsync(hr.scal, c->scal, sizeof(Scal) * c->B, cudaMemcpyDeviceToHost, c->st));
+  const bool want_hist = stats && stats->relres_hist;
+  if (want_hist)
+    CK(cudaMemcpyAsync(hr.hist, c->hist, (size_t)c->B * c->hist_stride * sizeof(float), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   if ((s = build_checked(c))) return s;
-  std::vector<Scal> hs(c->B);
-  CK(cudaMemcpy(hs.data(), c->scal, sizeof(Scal) * c->B, cudaMemcpyDeviceToHost));
+  std::vector<Scal> hs(hr.scal, hr.scal + c->B);
   if (c->timing) {
     if (kr) {
       std::vector<int32_t> it(c->B);
@@ -2001,11 +2044,7 @@ sb_status sb_pcg_solve(sb_ctx* c, const sb_c64* b, sb_c64* x, const sb_pcg_opts*
     c->launches += g0.nfixed + (int64_t)g0.nbody * ((mx + g0.unroll - 1) / g0.unroll);
   }
   if (stats) {
-    std::vector<float> hist;
-    if (stats->relres_hist) {
-      hist.resize((size_t)c->B * c->hist_stride);
-      CK(cudaMemcpy(hist.data(), c->hist, hist.size() * sizeof(float), cudaMemcpyDeviceToHost));
-    }
+    const float* hist = hr.hist;
     for (int i = 0; i < c->B; ++i) {
       if (stats->iters) stats->iters[i] = hs[i].iter;
       if (stats->converged) stats->converged[i] = (int8_t)hs[i].converged;
@@ -2015,7 +2054,7 @@ sb_status sb_pcg_solve(sb_ctx* c, const sb_c64* b, sb_c64* x, const sb_pcg_opts*
           stats->relres_hist[(size_t)i * (o->max_iters + 1) + k] = hist[(size_t)i * c->hist_stride + k];
     }
   }
-  return status_from_scal(c);
+  return status_of(c, hs.data());
 }
 
 sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* x_out, sb_recon_log* log) {
@@ -2026,9 +2065,11 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
   if ((s = check_opts(c, &ro->pcg))) return s;
   if ((s = ensure_hist(c, ro->pcg.max_iters, ro->n_outer))) return s;
   const size_t bytes = c->B * c->img * sizeof(float2), ybytes = bytes * c->C;
-  cudaEvent_t e0, e1;
-  CK(cudaEventCreate(&e0));
-  CK(cudaEventCreate(&e1));
+  if (!c->rev[0]) {
+    CK(cudaEventCreate(&c->rev[0]));
+    CK(cudaEventCreate(&c->rev[1]));
+  }
+  cudaEvent_t e0 = c->rev[0], e1 = c->rev[1];
   CK(cudaEventRecord(e0, c->st));
   // y is always copied into the context's staging buffer so the cached graphs stay valid
   if (!c->stage_in) CK(dalloc(&c->stage_in, c->B * c->C * c->img));
@@ -2079,17 +2120,21 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
   CK(cudaMemcpyAsync(x_out, c->x, bytes, is_device_ptr(x_out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                      c->st));
   CK(cudaEventRecord(e1, c->st));
+  HostRes hr;
+  if ((s = host_results(c, ro->n_outer, &hr))) return s;
+  const size_t nl = (size_t)ro->n_outer * c->B;
+  CK(cudaMemcpyAsync(hr.scal, c->scal, sizeof(Scal) * c->B, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(hr.iters, c->log_iters, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(hr.relres, c->log_relres, nl * sizeof(float), cudaMemcpyDeviceToHost, c->st));
+  if (kr) CK(cudaMemcpyAsync(hr.stamp, c->kstamp, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   if ((s = build_checked(c))) return s;
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   const bool stages = kr || c->stage_timing;
   stage_collect(c);
   if (kr) {  // the kernel's stage cycle counters, converted with its own cycles -> ns ratio
-    unsigned long long hst[32];
-    CK(cudaMemcpy(hst, c->kstamp, sizeof(hst), cudaMemcpyDeviceToHost));
+    const unsigned long long* hst = hr.stamp;
     if (getenv("SBPCG_KR_PROF") && atoi(getenv("SBPCG_KR_PROF")) == 2 && c->N <= 256) {  // skew probe dump
       std::vector<unsigned long long> pr(4 * 256);
       CK(cudaMemcpy(pr.data(), c->kstamp + 32, pr.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
@@ -2110,10 +2155,8 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
     c->stage_s[ST_SHRINK] += s_per_cyc * (double)hst[2];
   }
   c->stage_timing = false;
-  std::vector<int32_t> li((size_t)ro->n_outer * c->B);
-  std::vector<float> lr((size_t)ro->n_outer * c->B);
-  CK(cudaMemcpy(li.data(), c->log_iters, li.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(lr.data(), c->log_relres, lr.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  std::vector<int32_t> li(hr.iters, hr.iters + nl);
+  std::vector<float> lr(hr.relres, hr.relres + nl);
   if (c->timing) {
     if (kr) c->kr_alg_bytes += kr_bytes(c, li, ro->n_outer, true);
     timing_collect(c);
@@ -2138,7 +2181,7 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
     log->build_s = c->build_s;
     log->stages_valid = stages ? 1 : 0;
   }
-  return status_from_scal(c);
+  return status_of(c, hr.scal);
 }
 
 sb_status sb_sb_update3(sb_ctx* c, const sb_c64* x, sb_c64* bx, sb_c64* by, sb_c64* bz, sb_c64* bw,
