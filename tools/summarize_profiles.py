@@ -31,7 +31,7 @@ for cfg in (2, 3, 4, 5):
         mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         rd = float(g("dram__bytes_read.sum")[0].replace(",", "")) * mult.get(g("dram__bytes_read.sum")[1], 1)
         wr = float(g("dram__bytes_write.sum")[0].replace(",", "")) * mult.get(g("dram__bytes_write.sum")[1], 1)
-        traffic[f"config{cfg}"] = rd + wr
+        traffic[f"config{cfg}" + ("_kr" if "k_persist" in name else "")] = rd + wr
         stalls = sorted(((float(v[i].replace(",", "")), k[33:]) for i, k in enumerate(h)
                          if k.startswith("smsp__pcsamp_warps_issue_stalled") and not k.endswith("_not_issued")
                          and v[i] not in ("", "n/a")), reverse=True)
