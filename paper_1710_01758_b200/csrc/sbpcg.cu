@@ -1969,7 +1969,9 @@ static sb_status check_opts(sb_ctx* c, const sb_pcg_opts* o) {
     CK(dalloc(&c->jinv, (size_t)c->B * c->img));
     float* fr = nullptr;
     CK(dalloc(&fr, c->B));
-    CK(cudaMemcpy(fr, c->samp_frac.data(), c->B * sizeof(float), cudaMemcpyHostToDevice));
+    // on the context stream (a non-blocking caller stream does not order after the legacy one);
+    // samp_frac outlives the copy, and the stream is synchronised below
+    CK(cudaMemcpyAsync(fr, c->samp_frac.data(), c->B * sizeof(float), cudaMemcpyHostToDevice, c->st));
     CK(launch_jacobi_diag(c->sens, fr, c->B, c->C, c->img, c->ndim, c->mu, c->lam, c->gam, c->jinv, c->st));
     CK(cudaStreamSynchronize(c->st));
     cudaFree(fr);
