@@ -615,6 +615,10 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
         if (probe) a.stamp[32 + 4 * t] = gtime();
         // ---- z_kc = F0^H T (columns t-1, t, t+1), w = A z, W = F0 w ; rho, delta, ||r||^2
         double rz = kr_col_inv_z<M>(S, a.Tb, xl, twr, boff, t);
+        // x_kc to the image (the stores drain behind the data term; barrier A orders them), so a
+        // loop that stops after this pass's barrier A needs no solve-exit store and barrier
+        if (kc > 0)
+          for (int i = tid; i < M; i += NT) a.x[boff + (size_t)i * N + t] = S.xs[i];
         __syncthreads();
         seg(0);
         kr_dataterm<M, SMC>(S, S.zc[1], coils, sTb, C, xl, twr, mbits, minv);
@@ -905,10 +909,16 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
       seg(9);
     }
 
-    // ================= solve exit: x (own column) to the image, scalars and log
+    // ================= solve exit: x (own column) to the image, scalars and log.  The
+    // Chronopoulos-Gear loop stored x_kc at the start of every pass kc and stops after a barrier A
+    // (or before any update), and a solve that stopped in the prelude left x0 unchanged, so there
+    // only x = 0 (||b|| = 0) needs a store and the barrier before the SB step; the decision is
+    // uniform over the problem's CTAs.
     seg(-1);
-    for (int i = tid; i < M; i += NT)
-      a.x[boff + (size_t)i * N + t] = sc.zero_x ? make_float2(0.f, 0.f) : S.xs[i];
+    const bool xstore = !a.cg || sc.zero_x;
+    if (xstore)
+      for (int i = tid; i < M; i += NT)
+        a.x[boff + (size_t)i * N + t] = sc.zero_x ? make_float2(0.f, 0.f) : S.xs[i];
     if (lead && tid == 0) {
       Scal& g = a.L.scal[b];
       g.rho = sc.rho;
@@ -932,7 +942,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
 
     // ================= SB step (Alg. 1 steps 6-11 and the regulariser RHS), 16 x 16 tiles
     seg(15);
-    pbar(barc, target, P);  // x of every column visible
+    if (xstore) pbar(barc, target, P);  // x of every column visible (else ordered by barrier A)
     seg(16);
     {
       SbArgs sa = a.sb;
@@ -943,7 +953,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
       sa.by_out = a.bys[1 - par];
       constexpr int TT = Cf::TT;
       const int ntj = N / TT, ntile = (M / TT) * ntj;
-      for (int tile = t; tile < ntile; tile += P) sb_tile<TT, true, NT>(sa, S.u.sb, tile / ntj, tile % ntj, b);
+      for (int tile = t; tile < ntile; tile += P) sb_tile<TT, true, NT>(sa, S.u.sb, tile / ntj, tile % ntj, b, (timer && a.prof) ? a.stamp + 8 + 19 : nullptr);
     }
     seg(17);
     pbar(barc, target, P);  // rhs_reg, b_* visible to the next prelude

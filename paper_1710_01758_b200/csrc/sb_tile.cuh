@@ -28,8 +28,20 @@ __device__ __forceinline__ float2 shrinkc(float2 z, float t) {
 // index division below is a shift or a constant-divisor multiply (the kernel is issue bound).
 // One TT x TT tile (tile row ti, tile column tj) of problem b, with `nt` threads (all of the
 // CTA); also the SB phase of the persistent reconstruction kernel (k_persist.cu).
+// prof (nullable): phase cycle counters of the KR segment profile (SBPCG_KR_PROF=1), added by
+// thread 0 of the caller's profiled CTA: [0] load batch, [1] TV, [2] forward Haar, [3] shrink,
+// [4] inverse Haar + rhs
 template <int TT, bool FIX, int nt>
-__device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, int tj, int b) {
+__device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, int tj, int b,
+                                        unsigned long long* prof = nullptr) {
+  long long pc = prof ? clock64() : 0;
+  auto ph = [&](int k) {
+    if (prof) {
+      const long long c = clock64();
+      atomicAdd(prof + k, (unsigned long long)(c - pc));
+      pc = c;
+    }
+  };
   auto& xs = S.xs;
   auto& vx = S.vx;
   auto& vy = S.vy;
@@ -129,6 +141,7 @@ __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, 
     }
   }
   __syncthreads();
+  ph(0);
 
   if (do_tv) {
     // v_x at rows i0..i0+TH (TH+1), cols j0..j0+TW-1 ; v_y at rows i0..i0+TH-1, cols j0..j0+TW
@@ -156,6 +169,7 @@ __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, 
     }
   }
 
+  ph(1);
   if (do_w) {
     // forward Haar, tile-local Mallat layout in wa
     for (int e = tid; e < TH * TW; e += nt) wa[e / TW][e % TW] = xs[e / TW + 1][e % TW + 1];
@@ -190,6 +204,7 @@ __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, 
         __syncthreads();
       }
     }
+    ph(2);
     // shrink in the coefficient domain, b_w update at global Mallat positions (the old b_w was
     // parked in wv by the load batch; each thread reads and overwrites only its own cells)
     for (int e = tid; e < TH * TW; e += nt) {
@@ -203,6 +218,7 @@ __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, 
       wv[u][v] = make_float2(d.x - bn.x, d.y - bn.y);
     }
     __syncthreads();
+    ph(3);
     // inverse Haar of wv (coarsest level first)
     for (int lv = L; lv >= 1; --lv) {
       const int h0 = TH >> lv, h1 = TW >> lv;
@@ -249,6 +265,7 @@ __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, 
     a.rhs[boff + (size_t)(i0 + u) * N + (j0 + v)] = out;
   }
   __syncthreads();  // the tile's shared memory may be reused at once
+  ph(4);
 }
 
 }  // namespace sbk

@@ -2148,7 +2148,7 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
     }
     if (getenv("SBPCG_KR_PROF") && atoi(getenv("SBPCG_KR_PROF")) > 0) {  // loop segment profile (stderr)
       fprintf(stderr, "KR segments (ns, all iterations):");
-      for (int k = 0; k < 19; ++k) fprintf(stderr, " s%d=%.0f", k, hst[3] ? (double)hst[8 + k] * hst[4] / hst[3] : 0.0);
+      for (int k = 0; k < 24; ++k) fprintf(stderr, " s%d=%.0f", k, hst[3] ? (double)hst[8 + k] * hst[4] / hst[3] : 0.0);
       fprintf(stderr, "\n");
     }
     const double s_per_cyc = hst[3] > 0 ? 1e-9 * (double)hst[4] / (double)hst[3] : 0.0;
