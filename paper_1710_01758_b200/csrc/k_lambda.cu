@@ -288,6 +288,131 @@ cudaError_t launch_lambda_build(const LamArgs& a, cudaStream_t st) { return lam_
 cudaError_t launch_lambda_chunk(const LamArgs& a, cudaStream_t st) { return lam_mn<1>(a, st); }
 cudaError_t launch_lambda_tail(const LamArgs& a, cudaStream_t st) { return lam_mn<2>(a, st); }
 
+// ------------------------------------------------------------------ separable (line) masks
+// K4S: for a mask constant along d1 (r(nu0, nu1) = r0(nu0), the Cartesian lines of PAPER.md:265)
+// the correlation collapses to one dimension:
+//   k_c(nu0, nu1) = sum_{q0} r0(nu0 + q0) g0(q0),   g0(q0) = sum_{q1} g(q0, q1)
+//                 = (N1 / N^2) sum_c sum_{x1} |(D_0 s_c)(q0, x1)|^2      (Parseval along d1),
+// with D_0 the unnormalised length-M DFT down every column and N1 the row length, so the
+// build needs one fp64 column FFT per coil column (instead of C + 3 2D FFTs) and k_c depends on
+// nu0 only.  Exact (up to rounding) for separable masks; pinned by the same get_k parity tests.
+template <int M>
+__global__ void __launch_bounds__(LCol<M>::NT) k_lsep_col(const LamArgs a) {
+  using Cf = LCol<M>;
+  constexpr int N1 = Cf::N1;
+  __shared__ __align__(16) double2 xch[Cf::XS];
+  __shared__ double2 tw[M];
+  static_assert(M * (LW + 1) <= 2 * Cf::XS, "column partials fit the exchange buffer");
+  double (*red)[LW + 1] = reinterpret_cast<double (*)[LW + 1]>(xch);  // after the coil loop
+  const int tid = threadIdx.x, j = tid / LW, l = tid % LW;
+  const int N = a.N, S = a.csplit;
+  const int cta = blockIdx.x, sg = blockIdx.y, b = blockIdx.z;
+  const int col = cta * LW + l;
+  const size_t img = (size_t)M * N;
+  for (int i = tid; i < M; i += Cf::NT) tw[i] = a.tw_m[i];
+  __syncthreads();
+  const int per = (a.C + S - 1) / S, c0 = sg * per, c1 = min(a.C, c0 + per);
+  double acc[N1];
+#pragma unroll
+  for (int q = 0; q < N1; ++q) acc[q] = 0.0;
+  for (int c = c0; c < c1; ++c) {
+    const float2* sc = a.sens + ((size_t)b * a.C + c) * img;
+    double2 v[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const float2 f = sc[(size_t)natidx<M>(j, n1) * N + col];
+      v[n1] = make_double2(f.x, f.y);
+    }
+    fft_fwd<M, typename Cf::Lay>(v, xch, tw, j, l);
+#pragma unroll
+    for (int q = 0; q < N1; ++q) acc[q] += v[q].x * v[q].x + v[q].y * v[q].y;
+    __syncthreads();  // xch reused by the next coil
+  }
+#pragma unroll
+  for (int q = 0; q < N1; ++q) red[specidx<M>(j, q)][l] = acc[q];
+  __syncthreads();
+  // this CTA's LW columns summed in a fixed order -> gpart[b][sg][cta][q0]
+  const int nct = gridDim.x;
+  for (int q0 = tid; q0 < M; q0 += Cf::NT) {
+    double t = 0.0;
+#pragma unroll
+    for (int ll = 0; ll < LW; ++ll) t += red[q0][ll];
+    a.gpart[(((size_t)b * S + sg) * nct + cta) * M + q0] = t;
+  }
+}
+
+// g0(q0) for 32 consecutive q0 per CTA: thread (p, qq) sums partial rows p, p + 8, ... of the
+// (coil group, column tile) list for q0 = base + qq (coalesced loads, independent of each other),
+// then the 8 chains are added in a fixed order
+__global__ void __launch_bounds__(256) k_lsep_g0(const LamArgs a, int nrow) {
+  __shared__ double part[8][33];
+  const int M = a.M, N = a.N, b = blockIdx.y;
+  const int qq = threadIdx.x & 31, p = threadIdx.x >> 5, q0 = blockIdx.x * 32 + qq;
+  double t = 0.0;
+  if (q0 < M)
+    for (int r = p; r < nrow; r += 8) t += a.gpart[((size_t)b * nrow + r) * M + q0];
+  part[p][qq] = t;
+  __syncthreads();
+  if (p == 0 && q0 < M) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += part[k][qq];
+    const double img = (double)M * (double)N;
+    a.g[(size_t)b * M + q0].x = s * ((double)N / (img * img));
+  }
+}
+
+// one row nu0 per CTA: k_c(nu0) = sum_q g0(q) r0(nu0 + q) (fixed-order block sum), then
+// k = mu k_c + lambda (4 sin^2(pi nu0/M) + 4 sin^2(pi nu1/N)) + gamma and Lambda^{-1} = 1/(N k)
+// along the row
+__global__ void __launch_bounds__(256) k_lsep_expand(const LamArgs a) {
+  __shared__ double red[32];
+  const int M = a.M, N = a.N, row = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const int m = (a.nmask == 1) ? 0 : b;
+  double v = 0.0;
+  for (int q = tid; q < M; q += blockDim.x)
+    if (a.mask[(size_t)m * a.mask_bstride + (size_t)((row + q) % M) * N]) v += a.g[(size_t)b * M + q].x;
+  const double kc = block_sum(v, red);
+  if (tid == 0) red[0] = kc;
+  __syncthreads();
+  const double kcr = red[0];
+  const size_t img = (size_t)M * N;
+  const double PI = 3.14159265358979323846;
+  const double sr = sin(PI * (double)row / (double)M);
+  for (int col = tid; col < N; col += blockDim.x) {
+    const double sc = sin(PI * (double)col / (double)N);
+    const double k = a.mu * kcr + a.lam * (4.0 * sr * sr + 4.0 * sc * sc) + a.gam;
+    const size_t gi = (size_t)b * img + (size_t)row * N + col;
+    a.k_out[gi] = k;
+    if (!(fabs(k) > 1e-14) || !isfinite(k)) atomicExch(a.bad, 1);
+    a.lam_inv[gi] = (float)(1.0 / ((double)img * k));
+  }
+}
+
+template <int M>
+static cudaError_t lsep_m(const LamArgs& a, cudaStream_t st) {
+  const int nct = a.N / LW;
+  k_lsep_col<M><<<dim3(nct, a.csplit, a.B), LCol<M>::NT, 0, st>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_lsep_g0<<<dim3((M + 31) / 32, a.B), 256, 0, st>>>(a, a.csplit * nct);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k_lsep_expand<<<dim3(M, a.B), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// csplit coil groups, gpart >= B * csplit * (N / 8) * M doubles, g >= B * M (g0 in .x)
+cudaError_t launch_lambda_sep(const LamArgs& a, cudaStream_t st) {
+  if (a.N % LW != 0) return cudaErrorInvalidValue;
+  switch (a.M) {
+#define X(m_) \
+  case m_: return lsep_m<m_>(a, st);
+    SBK_LAM_SIZES(X)
+#undef X
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_lexpand3(const Lam3Args a) {
   const size_t pn = (size_t)a.D1 * a.D2, img = pn * a.D0;
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -96,6 +96,7 @@ struct LamArgs {
   double* kc2;             // [B][D1*D2]
 };
 
+cudaError_t launch_lambda_sep(const LamArgs& a, cudaStream_t st);  // separable (line) masks, K4S
 // 3D Lambda: k[x][y][z] = mu kc2[y][z] / D0 + lambda sum_d 4 sin^2(pi nu_d/n_d) + gamma,
 // Lambda^{-1} = 1/(N k)
 struct Lam3Args {

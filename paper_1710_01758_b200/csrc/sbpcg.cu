@@ -1149,6 +1149,26 @@ static sb_status build_lambda_impl(sb_ctx* c) {
   a.tw_n = c->twd_n;
   double2 *tmp = nullptr, *g = nullptr, *rh = nullptr;
   int* bad = nullptr;
+  if (c->separable && env_flag("SBPCG_LSEP", true)) {
+    // line masks: the one-dimensional form (k_lambda.cu K4S), three launches.  Coil groups
+    // split the column pass when the batch alone leaves SMs idle.
+    const int nct = c->N / 8;
+    int S = std::max(1, std::min(c->C, (2 * 148 + c->B * nct - 1) / (c->B * nct)));
+    const int per = (c->C + S - 1) / S;
+    S = (c->C + per - 1) / per;
+    double* gpart = nullptr;
+    CK(lscratch(c, 3, &bad, 1));
+    CK(lscratch(c, 1, &g, (size_t)c->B * c->M));
+    CK(lscratch(c, 5, &gpart, (size_t)c->B * S * nct * c->M));
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), c->st));
+    a.bad = bad;
+    a.csplit = S;
+    a.gpart = gpart;
+    a.g = g;
+    CK(launch_lambda_sep(a, c->st));
+    c->launches += 3;
+    return finish_lambda(c, nullptr, nullptr, nullptr, bad, nullptr);
+  }
   CK(lscratch(c, 0, &tmp, (size_t)c->B * c->C * c->img));
   CK(lscratch(c, 1, &g, (size_t)c->B * c->img));
   CK(lscratch(c, 2, &rh, (size_t)a.nmask * c->img));

@@ -335,3 +335,25 @@ def test_singular_k_reporting():
     x, log = ctx.recon(y, 1, eps=0.0, max_iters=2)
     assert torch.isfinite(x).all()
     ctx.close()
+
+
+@pytest.mark.parametrize("shape,coils,nb", [((256, 256), 12, 1), ((64, 64), 4, 3), ((8, 8), 2, 2), ((128, 32), 5, 1)],
+                         ids=["256c12b1", "64c4b3", "8c2b2", "128x32c5b1"])
+def test_separable_lambda_build_equals_2d_build(monkeypatch, shape, coils, nb):
+    """K4S (k_lambda.cu: the one-dimensional form of k_c for line masks, Parseval along d1)
+    against the general 2D correlation build (C + 3 2D FFTs) on the same maps, both fp64 on the
+    device: equal to rounding.  The oracle pin of both is test_apply_A_and_Pinv_and_k."""
+    ps = batch(2, nb, shape, coils)
+    mu, lam, gam = 1.0, 0.02, 0.02
+    monkeypatch.setenv("SBPCG_LSEP", "1")
+    ctx = _ctx(ps, mu, lam, gam, 1)
+    k_sep = ctx.get_k().numpy()
+    ctx.close()
+    monkeypatch.setenv("SBPCG_LSEP", "0")
+    ctx = _ctx(ps, mu, lam, gam, 1)
+    k_2d = ctx.get_k().numpy()
+    ctx.close()
+    assert np.max(np.abs(k_sep - k_2d) / np.abs(k_2d)) <= 1e-12
+    for b, p in enumerate(ps):
+        kref = precond.build_k(p["sens"].astype(np.complex64).astype(np.complex128), p["mask"], mu, lam, gam)
+        assert relerr(k_sep[b], kref) <= 1e-6
