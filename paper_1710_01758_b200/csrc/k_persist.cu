@@ -155,6 +155,21 @@ __device__ __forceinline__ void psum(const double* part, double* bc) {
   __syncthreads();
 }
 
+// psum<P, 1> by the calling warp (any warp), result in *dst (lane 0); no block barrier.
+template <int P>
+__device__ __forceinline__ void psum1_warp(const double* part, double* dst) {
+  constexpr int K = P / 64;
+  const int lane = threadIdx.x & 31;
+  double2 v[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) v[i] = __ldcg(reinterpret_cast<const double2*>(part) + lane + 32 * i);
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) acc += v[i].x + v[i].y;
+  acc = warp_sum(acc);
+  if (lane == 0) *dst = acc;
+}
+
 // Two deterministic block sums at once (fixed shuffle tree, fixed warp order); thread 0.
 __device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -614,12 +629,27 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
         };
         if (probe) a.stamp[32 + 4 * t] = gtime();
         // ---- z_kc = F0^H T (columns t-1, t, t+1), w = A z, W = F0 w ; rho, delta, ||r||^2
-        double rz = kr_col_inv_z<M>(S, a.Tb, xl, twr, boff, t);
-        // x_kc to the image (the stores drain behind the data term; barrier A orders them), so a
-        // loop that stops after this pass's barrier A needs no solve-exit store and barrier
-        if (kc > 0)
-          for (int i = tid; i < M; i += NT) a.x[boff + (size_t)i * N + t] = S.xs[i];
+        double rz = kr_col_inv_z<M>(S, a.Tb, xl, twr, boff, t);  // warps 0-1
+        // ||r_kc||^2 (slot 6, published before the last barrier B), summed by the last warp
+        // while the first ones transform T: the stop test on ||r_kc|| / ||b|| runs before the
+        // data term, so the pass that would only confirm convergence is not computed
+        if (kc > 0 && tid >= NT - 32) psum1_warp<P>(part + 6 * P, &S.bc[7]);
         __syncthreads();
+        if (kc > 0) {  // checks of iteration kc on ||r_kc|| (fin_rr order)
+          const double rr = S.bc[7];
+          sc.rr = rr;
+          sc.iter = kc;
+          const double rel = sqrt(rr / sc.nb2);
+          hist_put(kc, rel);
+          if (!isfinite(rr)) {
+            sc.status = ST_NONFINITE;
+            break;
+          }
+          if (a.eps > 0.f && rel <= (double)a.eps) {
+            sc.converged = 1;
+            break;
+          }
+        }
         seg(0);
         kr_dataterm<M, SMC>(S, S.zc[1], coils, sTb, C, xl, twr, mbits, minv);
         seg(1);
@@ -662,20 +692,8 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
         for (int e = tid; e < N / 2; e += NT) kr_cp16(S.wrow + 2 * e, a.Qs + boff + (size_t)t * N + 2 * e);
         kr_cp_commit();
         psum<P, 6>(part, S.bc);
-        const double rho = S.bc[0], delta = S.bc[1], rr = S.bc[2], zs_ = S.bc[3], pw_ = S.bc[4], ps_ = S.bc[5];
-        if (kc >= 1) {  // checks of iteration kc (fin_rr, fin_rho order)
-          sc.rr = rr;
-          sc.iter = kc;
-          const double rel = sqrt(rr / sc.nb2);
-          hist_put(kc, rel);
-          if (!isfinite(rr)) {
-            sc.status = ST_NONFINITE;
-            break;
-          }
-          if (a.eps > 0.f && rel <= (double)a.eps) {
-            sc.converged = 1;
-            break;
-          }
+        const double rho = S.bc[0], delta = S.bc[1], zs_ = S.bc[3], pw_ = S.bc[4], ps_ = S.bc[5];
+        if (kc >= 1) {  // checks of iteration kc (fin_rho order; the ||r_kc|| ones ran above)
           if (!isfinite(rho)) {
             sc.status = ST_NONFINITE;
             break;
@@ -715,7 +733,8 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
         seg(4);
         const float fb = (float)beta, fa = (float)sc.alpha;
         const bool first = kc == 0;
-        // column t: p = z + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s
+        // column t: p = z + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s ; ||r||^2
+        double drn = 0.0;
         for (int i = tid; i < M; i += NT) {
           const float2 z = S.zc[1][i], w = S.qs[i];
           float2 pp = z, sv = w;
@@ -727,9 +746,17 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
           S.pc[1][i] = pp;
           S.ss[i] = sv;
           const float2 x = S.xs[i], r0 = S.rs[i];
-          S.xs[i] = make_float2(x.x + fa * pp.x, x.y + fa * pp.y);
-          S.rs[i] = make_float2(r0.x - fa * sv.x, r0.y - fa * sv.y);
+          const float2 xn = make_float2(x.x + fa * pp.x, x.y + fa * pp.y);
+          S.xs[i] = xn;
+          // x_{k+1} to the image now (ordered by this pass's barrier B): a loop that stops at the
+          // start of the next pass, or after its barrier A, needs no solve-exit store + barrier
+          a.x[boff + (size_t)i * N + t] = xn;
+          const float2 rn = make_float2(r0.x - fa * sv.x, r0.y - fa * sv.y);
+          S.rs[i] = rn;
+          drn += (double)rn.x * rn.x + (double)rn.y * rn.y;
         }
+        drn = warp_sum(drn);
+        if ((tid & 31) == 0) S.red[40 + (tid >> 5)] = drn;  // (phase C's slot-5 sums are consumed)
         // row t: S_s = W + beta S_s ; S_r -= alpha S_s ; T = F1^H Lambda^{-1} F1 S_r
         kr_cp_wait();
         __syncthreads();  // every thread's part of the W row has landed
@@ -762,6 +789,11 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
 #pragma unroll
             for (int n1 = 0; n1 < N1_; ++n1) tt[(size_t)(N2 * n1 + j) * M] = v[n1];
           }
+        } else if (tid == 32) {  // ||r_{k+1}||^2 partial of this column (slot 6), fixed warp order
+          double sr = 0.0;
+#pragma unroll
+          for (int w = 0; w < NT / 32; ++w) sr += S.red[40 + w];
+          part[6 * P + t] = sr;
         }
         seg(5);
         pbar(barc, target, P);
@@ -910,8 +942,8 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
     }
 
     // ================= solve exit: x (own column) to the image, scalars and log.  The
-    // Chronopoulos-Gear loop stored x_kc at the start of every pass kc and stops after a barrier A
-    // (or before any update), and a solve that stopped in the prelude left x0 unchanged, so there
+    // Chronopoulos-Gear loop stored every x_k before the barrier B that ends its pass (it stops
+    // after a barrier B or A), and a solve that stopped in the prelude left x0 unchanged, so there
     // only x = 0 (||b|| = 0) needs a store and the barrier before the SB step; the decision is
     // uniform over the problem's CTAs.
     seg(-1);
