@@ -489,13 +489,19 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
 
     // ================= prelude: r0 = b - A x0 (+ RHS and data feedback) ; S_r = F0 r0
     seg(-1);
-    {  // one load batch: x of columns t-1, t, t+1 and u, u1, rhs_reg (or b) of column t
+    {  // one load batch: x of columns t-1, t, t+1 and u, u1, rhs_reg (or b) of column t.  After
+      // the first solve x comes from the column-major copy xT and rhs_reg is column-major (the SB
+      // step writes it so), so those reads are contiguous; u and u1 of the own column stay in
+      // shared memory across the solves (loaded from the image once).
       constexpr int E = (3 * M + NT - 1) / NT, EO = (M + NT - 1) / NT;
+      const bool xt = js > 0;
       float2 xv[E], uv[EO], u1v[EO], rv[EO];
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         const int e = tid + k * NT;
-        if (e < 3 * M) xv[k] = __ldcg(a.x + boff + (size_t)(e % M) * N + (t + e / M - 1 + N) % N);
+        const int col = (t + e / M - 1 + N) % N;
+        if (e < 3 * M)
+          xv[k] = __ldcg(xt ? a.xT + boff + (size_t)col * M + e % M : a.x + boff + (size_t)(e % M) * N + col);
       }
 #pragma unroll
       for (int k = 0; k < EO; ++k) {
@@ -503,10 +509,10 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
         if (i < M) {
           const size_t gi = boff + (size_t)i * N + t;
           if (recon) {
-            uv[k] = __ldcg(a.u + gi);
+            if (js == 0) uv[k] = __ldcg(a.u + gi);
             if (update_u) {
-              u1v[k] = __ldcg(a.u1 + gi);
-              rv[k] = __ldcg(a.rhs + gi);
+              if (js == 1) u1v[k] = __ldcg(a.u1 + gi);
+              rv[k] = __ldcg(a.rhs + boff + (size_t)t * M + i);
             }
           } else {
             rv[k] = __ldcg(a.bvec + gi);
@@ -518,7 +524,10 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
         const int e = tid + k * NT;
         if (e < 3 * M) {
           S.pc[e / M][e % M] = xv[k];
-          if (e / M == 1) S.xs[e % M] = xv[k];
+          if (e / M == 1) {
+            S.xs[e % M] = xv[k];
+            if (!xt) a.xT[boff + (size_t)t * M + e % M] = xv[k];  // x0 -> xT (the SB step reads it)
+          }
         }
       }
 #pragma unroll
@@ -526,9 +535,9 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
         const int i = tid + k * NT;
         if (i < M) {
           if (recon) {
-            S.ub[i] = uv[k];
+            if (js == 0) S.ub[i] = uv[k];
             if (update_u) {
-              S.u1b[i] = u1v[k];
+              if (js == 1) S.u1b[i] = u1v[k];
               S.rhb[i] = rv[k];
             }
           } else {
@@ -550,10 +559,10 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
       float2 bb;
       if (recon) {
         float2 uu = S.ub[i];
-        if (update_u) {  // u_{j+1} = u_j + u_1 - E^H E x (reading A28)
+        if (update_u) {  // u_{j+1} = u_j + u_1 - E^H E x (reading A28); kept in shared memory
           const float2 u1 = S.u1b[i];
           uu = make_float2(uu.x + u1.x - av.x, uu.y + u1.y - av.y);
-          a.u[gi] = uu;
+          S.ub[i] = uu;
         }
         const float2 rr = update_u ? S.rhb[i] : make_float2(0.f, 0.f);
         bb = make_float2(a.mu * uu.x + rr.x, a.mu * uu.y + rr.y);
@@ -750,7 +759,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
           S.xs[i] = xn;
           // x_{k+1} to the image now (ordered by this pass's barrier B): a loop that stops at the
           // start of the next pass, or after its barrier A, needs no solve-exit store + barrier
-          a.x[boff + (size_t)i * N + t] = xn;
+          a.xT[boff + (size_t)t * M + i] = xn;
           const float2 rn = make_float2(r0.x - fa * sv.x, r0.y - fa * sv.y);
           S.rs[i] = rn;
           drn += (double)rn.x * rn.x + (double)rn.y * rn.y;
@@ -946,11 +955,16 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
     // after a barrier B or A), and a solve that stopped in the prelude left x0 unchanged, so there
     // only x = 0 (||b|| = 0) needs a store and the barrier before the SB step; the decision is
     // uniform over the problem's CTAs.
+    // The image-layout x (the caller's output) is written by the last solve only.
     seg(-1);
     const bool xstore = !a.cg || sc.zero_x;
-    if (xstore)
-      for (int i = tid; i < M; i += NT)
-        a.x[boff + (size_t)i * N + t] = sc.zero_x ? make_float2(0.f, 0.f) : S.xs[i];
+    const bool xout = !recon || js == n_solves - 1;
+    if (xstore || xout)
+      for (int i = tid; i < M; i += NT) {
+        const float2 v = sc.zero_x ? make_float2(0.f, 0.f) : S.xs[i];
+        if (xstore) a.xT[boff + (size_t)t * M + i] = v;
+        if (xout) a.x[boff + (size_t)i * N + t] = v;
+      }
     if (lead && tid == 0) {
       Scal& g = a.L.scal[b];
       g.rho = sc.rho;
@@ -978,6 +992,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
     seg(16);
     {
       SbArgs sa = a.sb;
+      sa.x = a.xT;  // column-major x in, column-major rhs_reg out (CM)
       const int par = js & 1;
       sa.bx_in = a.bxs[par];
       sa.by_in = a.bys[par];
@@ -985,7 +1000,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
       sa.by_out = a.bys[1 - par];
       constexpr int TT = Cf::TT;
       const int ntj = N / TT, ntile = (M / TT) * ntj;
-      for (int tile = t; tile < ntile; tile += P) sb_tile<TT, true, NT>(sa, S.u.sb, tile / ntj, tile % ntj, b, (timer && a.prof) ? a.stamp + 8 + 19 : nullptr);
+      for (int tile = t; tile < ntile; tile += P) sb_tile<TT, true, NT, true>(sa, S.u.sb, tile / ntj, tile % ntj, b, (timer && a.prof) ? a.stamp + 8 + 19 : nullptr);
     }
     seg(17);
     pbar(barc, target, P);  // rhs_reg, b_* visible to the next prelude

@@ -143,7 +143,8 @@ struct KrArgs {
   const float2* bvec;        // solve mode: b
   float2* u;                 // recon: running u_j
   const float2* u1;
-  float2* rhs;               // recon: rhs_reg (written by the SB phase)
+  float2* rhs;               // recon: rhs_reg (written by the SB phase, column-major [B][N][M])
+  float2* xT;                // x, column-major [B][N][M] (internal; the image-layout x is the output)
   SbArgs sb;                 // recon: SB state (bx/by double buffers, bw, rhs), parity 0 first
   float2* bxs[2];
   float2* bys[2];

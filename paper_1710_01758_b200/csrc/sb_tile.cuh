@@ -8,13 +8,15 @@ namespace sbk {
 
 constexpr int SBT = 32;  // max tile edge
 
+// rows padded to an odd number of 8-byte cells: the column-order loops of the CM variant read
+// vx, wv down columns without bank conflicts
 template <int TT>
 struct SbTile {
   float2 xs[TT + 2][TT + 2];
-  float2 vx[TT + 1][TT];
+  float2 vx[TT + 1][TT + 1];
   float2 vy[TT][TT + 1];
-  float2 wa[TT][TT];
-  float2 wv[TT][TT];
+  float2 wa[TT][TT + 1];
+  float2 wv[TT][TT + 1];
 };
 
 __device__ __forceinline__ float2 shrinkc(float2 z, float t) {
@@ -31,7 +33,10 @@ __device__ __forceinline__ float2 shrinkc(float2 z, float t) {
 // prof (nullable): phase cycle counters of the KR segment profile (SBPCG_KR_PROF=1), added by
 // thread 0 of the caller's profiled CTA: [0] load batch, [1] TV, [2] forward Haar, [3] shrink,
 // [4] inverse Haar + rhs
-template <int TT, bool FIX, int nt>
+// CM: x is read from, and rhs written to, column-major images [B][N][M] (the persistent kernel's
+// layout, whose column owners then read them contiguously); the element loops of those two run
+// rows fastest so the accesses stay coalesced.  b_x, b_y, b_w keep the image layout.
+template <int TT, bool FIX, int nt, bool CM = false>
 __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, int tj, int b,
                                         unsigned long long* prof = nullptr) {
   long long pc = prof ? clock64() : 0;
@@ -94,9 +99,9 @@ __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, 
   for (int k = 0; k < KX; ++k) {
     const int e = tid + k * nt;
     if (e < (TH + 2) * (TW + 2)) {
-      const int u = e / (TW + 2), v = e % (TW + 2);
+      const int u = CM ? e % (TH + 2) : e / (TW + 2), v = CM ? e / (TH + 2) : e % (TW + 2);
       const int gi = (i0 + u - 1 + M) % M, gj = (j0 + v - 1 + N) % N;
-      rx[k] = __ldcg(a.x + boff + (size_t)gi * N + gj);
+      rx[k] = __ldcg(a.x + boff + (CM ? (size_t)gj * M + gi : (size_t)gi * N + gj));
     }
   }
   if (do_tv) {
@@ -123,7 +128,10 @@ __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, 
 #pragma unroll
   for (int k = 0; k < KX; ++k) {
     const int e = tid + k * nt;
-    if (e < (TH + 2) * (TW + 2)) xs[e / (TW + 2)][e % (TW + 2)] = rx[k];
+    if (e < (TH + 2) * (TW + 2)) {
+      if constexpr (CM) xs[e % (TH + 2)][e / (TH + 2)] = rx[k];
+      else xs[e / (TW + 2)][e % (TW + 2)] = rx[k];
+    }
   }
   if (do_tv) {
 #pragma unroll
@@ -251,7 +259,7 @@ __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, 
   __syncthreads();
 
   for (int e = tid; e < TH * TW; e += nt) {
-    const int u = e / TW, v = e % TW;
+    const int u = CM ? e % TH : e / TW, v = CM ? e / TH : e % TW;
     float2 out = make_float2(0.f, 0.f);
     if (do_tv) {
       const float2 a0 = vx[u][v], a1 = vx[u + 1][v], c0 = vy[u][v], c1 = vy[u][v + 1];
@@ -262,7 +270,7 @@ __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, 
       out.x += a.gam * wv[u][v].x;
       out.y += a.gam * wv[u][v].y;
     }
-    a.rhs[boff + (size_t)(i0 + u) * N + (j0 + v)] = out;
+    a.rhs[boff + (CM ? (size_t)(j0 + v) * M + (i0 + u) : (size_t)(i0 + u) * N + (j0 + v))] = out;
   }
   __syncthreads();  // the tile's shared memory may be reused at once
   ph(4);

@@ -1011,6 +1011,7 @@ static sb_status run_kr(sb_ctx* c, int n_outer, const sb_pcg_opts* o, int par0) 
   a.u = c->u;
   a.u1 = c->u1;
   a.rhs = c->rhs;
+  a.xT = c->z;  // free on the persistent path
   a.sb.B = c->B;
   a.sb.M = c->M;
   a.sb.N = c->N;
