@@ -67,6 +67,7 @@ struct KrSmem {
   float2 ssrow[M];                    // row t of S_s = F_0 s (Chronopoulos-Gear loop)
   float2 wrow[M];                     // row t of W = F_0 w (cp.async prefetch after the barrier)
   float2 ub[M], u1b[M], rhb[M];       // prelude: u, u1, rhs_reg (or b) of the own column
+  alignas(16) float2 sbpre[sb_pre_size<C::TT>()];  // recon: the SB tile's old b_x, b_y, b_w (cp.async in the prelude)
   float2 tw[M];
   float li[M];                        // Lambda^{-1} of spectral row t
   float rm[M];                        // r/M (row mask)
@@ -489,6 +490,16 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
 
     // ================= prelude: r0 = b - A x0 (+ RHS and data feedback) ; S_r = F0 r0
     seg(-1);
+    constexpr int TT = Cf::TT;
+    const int ntj = N / TT, ntile = (M / TT) * ntj;
+    const bool sbpre = recon && ntile <= P;  // one SB tile per CTA: stage its b_* now
+    const int par = js & 1;
+    if (sbpre && t < ntile) {
+      SbArgs sa = a.sb;
+      sa.bx_in = a.bxs[par];
+      sa.by_in = a.bys[par];
+      sb_tile_prefetch<TT, NT>(sa, S.sbpre, t / ntj, t % ntj, b);
+    }
     {  // one load batch: x of columns t-1, t, t+1 and u, u1, rhs_reg (or b) of column t.  After
       // the first solve x comes from the column-major copy xT and rhs_reg is column-major (the SB
       // step writes it so), so those reads are contiguous; u and u1 of the own column stay in
@@ -584,6 +595,9 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
     seg(12);
     pbar(barc, target, P);
     seg(13);
+    // row t of S_r for the solve's first row pass: its L2 round trip overlaps the all-reduce
+    for (int e = tid; e < N / 2; e += NT) kr_cp16(S.srow + 2 * e, a.Sr + boff + (size_t)t * N + 2 * e);
+    kr_cp_commit();
     psum<P, 2>(part, S.bc);
     {
       const double nb2 = S.bc[0], rr = S.bc[1];
@@ -612,6 +626,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
     }
     seg(14);
     stamp(0);
+    if (!sc.active) kr_cp_wait();  // no row pass follows: retire the S_r row copy
 
     if (sc.active && a.cg) {
       // ================= Chronopoulos-Gear PCG: the same
@@ -621,7 +636,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
       // iteration needs two barriers:  [z = M^{-1} r (column IFFTs), w = A z, W = F0 w,
       // partials] | barrier | [p, s, x, r updates; S_s = W + beta S_s, S_r -= alpha S_s; row
       // FFTs of M^{-1}] | barrier.
-      for (int i = tid; i < N; i += NT) S.srow[i] = __ldcg(a.Sr + boff + (size_t)t * N + i);
+      kr_cp_wait();  // row t of S_r (issued after the prelude barrier)
       __syncthreads();
       kr_row_pass<M>(a, S, xl, twr, boff, t, 0.f, false);
       pbar(barc, target, P);
@@ -811,7 +826,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
       sc.active = 0;
     } else if (sc.active) {
       // ================= z0 = M^{-1} r0 ; rho0 = Re<r0, z0>
-      for (int i = tid; i < N; i += NT) S.srow[i] = __ldcg(a.Sr + boff + (size_t)t * N + i);
+      kr_cp_wait();  // row t of S_r (issued after the prelude barrier)
       __syncthreads();
       kr_row_pass<M>(a, S, xl, twr, boff, t, 0.f, false);
       pbar(barc, target, P);
@@ -993,14 +1008,13 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
     {
       SbArgs sa = a.sb;
       sa.x = a.xT;  // column-major x in, column-major rhs_reg out (CM)
-      const int par = js & 1;
       sa.bx_in = a.bxs[par];
       sa.by_in = a.bys[par];
       sa.bx_out = a.bxs[1 - par];
       sa.by_out = a.bys[1 - par];
-      constexpr int TT = Cf::TT;
-      const int ntj = N / TT, ntile = (M / TT) * ntj;
-      for (int tile = t; tile < ntile; tile += P) sb_tile<TT, true, NT, true>(sa, S.u.sb, tile / ntj, tile % ntj, b, (timer && a.prof) ? a.stamp + 8 + 19 : nullptr);
+      for (int tile = t; tile < ntile; tile += P)
+        sb_tile<TT, true, NT, true>(sa, S.u.sb, tile / ntj, tile % ntj, b, (timer && a.prof) ? a.stamp + 8 + 19 : nullptr,
+                                    sbpre ? S.sbpre : nullptr);
     }
     seg(17);
     pbar(barc, target, P);  // rhs_reg, b_* visible to the next prelude

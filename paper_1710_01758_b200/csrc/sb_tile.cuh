@@ -36,9 +36,14 @@ __device__ __forceinline__ float2 shrinkc(float2 z, float t) {
 // CM: x is read from, and rhs written to, column-major images [B][N][M] (the persistent kernel's
 // layout, whose column owners then read them contiguously); the element loops of those two run
 // rows fastest so the accesses stay coalesced.  b_x, b_y, b_w keep the image layout.
+// pre (nullable, with CM): the tile's old b_x, b_y, b_w already staged in shared memory by
+// sb_tile_prefetch (cp.async issued earlier by the same threads), so the load batch is x only.
+template <int TT>
+constexpr int sb_pre_size() { return (TT + 1) * TT + TT * (TT + 2) + TT * TT; }  // b_y rows padded to even
+
 template <int TT, bool FIX, int nt, bool CM = false>
 __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, int tj, int b,
-                                        unsigned long long* prof = nullptr) {
+                                        unsigned long long* prof = nullptr, const float2* pre = nullptr) {
   long long pc = prof ? clock64() : 0;
   auto ph = [&](int k) {
     if (prof) {
@@ -104,7 +109,7 @@ __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, 
       rx[k] = __ldcg(a.x + boff + (CM ? (size_t)gj * M + gi : (size_t)gi * N + gj));
     }
   }
-  if (do_tv) {
+  if (do_tv && pre == nullptr) {
 #pragma unroll
     for (int k = 0; k < KV; ++k) {
       const int e = tid + k * nt;
@@ -118,11 +123,26 @@ __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, 
       }
     }
   }
-  if (do_w) {
+  if (do_w && pre == nullptr) {
 #pragma unroll
     for (int k = 0; k < KB; ++k) {
       const int e = tid + k * nt;
       if (e < TH * TW) rbw[k] = __ldcg(a.bw + mallat_gi(e / TW, e % TW));
+    }
+  }
+  if (pre != nullptr) {  // every thread's staged copies have landed, then visible to all
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+      const int e = tid + k * nt;
+      if (e < (TH + 1) * TW) rvx[k] = pre[e];
+      if (e < TH * (TW + 1)) rvy[k] = pre[(TT + 1) * TT + (e / (TT + 1)) * (TT + 2) + e % (TT + 1)];
+    }
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+      const int e = tid + k * nt;
+      if (e < TH * TW) rbw[k] = pre[(TT + 1) * TT + TT * (TT + 2) + e];
     }
   }
 #pragma unroll
@@ -274,6 +294,63 @@ __device__ __forceinline__ void sb_tile(const SbArgs& a, SbTile<TT>& S, int ti, 
   }
   __syncthreads();  // the tile's shared memory may be reused at once
   ph(4);
+}
+
+// Stage the old b_x, b_y (with their halo row / column) and b_w (Mallat positions) of tile
+// (ti, tj) into pre[sb_pre_size<TT>()] (FIX tiles only; pre 16-byte aligned): layout b_x
+// [TT+1][TT], b_y [TT][TT+2] (TT+1 used), b_w [TT][TT] in the order sb_tile's load batch uses.
+template <int TT, int nt>
+__device__ __forceinline__ void sb_tile_prefetch(const SbArgs& a, float2* pre, int ti, int tj, int b) {
+  // 16-byte copies of aligned element pairs (tile columns start at multiples of TT, and every
+  // Mallat run of a tile starts at an even column); b_y's halo column is one 8-byte copy per row
+  const int M = a.M, N = a.N, L = a.levels;
+  const int i0 = ti * TT, j0 = tj * TT;
+  const size_t boff = (size_t)b * M * N;
+  constexpr int H = TT / 2;                        // pairs per tile row
+  constexpr int NX = (TT + 1) * H, NY = TT * H, NW = TT * H;
+  for (int e = threadIdx.x; e < NX + NY + TT + NW; e += nt) {
+    const float2* src;
+    float2* dst;
+    bool pair = true;
+    if (e < NX) {
+      const int u = e / H, v = 2 * (e % H);
+      src = a.bx_in + boff + (size_t)((i0 + u) % M) * N + j0 + v;
+      dst = pre + u * TT + v;
+    } else if (e < NX + NY) {
+      const int f = e - NX, u = f / H, v = 2 * (f % H);
+      src = a.by_in + boff + (size_t)(i0 + u) * N + j0 + v;
+      dst = pre + (TT + 1) * TT + u * (TT + 2) + v;
+    } else if (e < NX + NY + TT) {  // b_y halo column j0 + TT (periodic)
+      const int u = e - NX - NY;
+      src = a.by_in + boff + (size_t)(i0 + u) * N + (j0 + TT) % N;
+      dst = pre + (TT + 1) * TT + u * (TT + 2) + TT;
+      pair = false;
+    } else {
+      const int f = e - NX - NY - TT, u = f / H, v = 2 * (f % H);
+      int lv = 1, hi0 = 0, hi1 = 0, ca = u, cb = v;
+      bool ll = true;
+      for (; lv <= L; ++lv) {
+        const int h0 = TT >> lv, h1 = TT >> lv;
+        if (u < h0 && v < h1) continue;
+        hi0 = u >= h0;
+        hi1 = v >= h1;
+        ca = u - hi0 * h0;
+        cb = v - hi1 * h1;
+        ll = false;
+        break;
+      }
+      const int gu = ll ? (i0 >> L) + u : (hi0 ? (M >> lv) : 0) + (i0 >> lv) + ca;
+      const int gv = ll ? (j0 >> L) + v : (hi1 ? (N >> lv) : 0) + (j0 >> lv) + cb;
+      src = a.bw + boff + (size_t)gu * N + gv;
+      dst = pre + (TT + 1) * TT + TT * (TT + 2) + u * TT + v;
+    }
+    if (pair) {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+    } else {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 }  // namespace sbk
