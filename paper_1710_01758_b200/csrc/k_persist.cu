@@ -74,7 +74,7 @@ struct KrSmem {
   double red[48];
   double bc[8];                       // broadcast of reduced scalars
   long long tclk, tclk0;              // stage timer state (one thread of one CTA)
-  unsigned long long tgt0, tstage[3];
+  unsigned long long tgt0, tstage[4];  // rhs, pcg, shrink, init
   // followed (SMC) by the coil-map column lines [C][M]
 };
 
@@ -394,6 +394,104 @@ __device__ __forceinline__ double kr_col_inv_z(KrSmem<M>& S, const float2* Tb, f
   return rz;
 }
 
+// Alg. 1 step 1 inside the launch (recon, KrArgs::kinit): u1 = sum_c S_c^H F^H y_c and the
+// root-sum-of-squares start x1 = sqrt(sum_c |F^H y_c|^2) (reading A12), with F the
+// unitary 2D DFT and y zero-filled k-space masked by R (rows of a line mask).  Phase 1 (row t):
+// the length-N inverse DFT of row t of every coil's k-space into Y1T (column-major, one line
+// per coil, LPAR coils at a time).  Phase 2 (column t, after a barrier): the length-M inverse
+// DFT of column t of every Y1T, the coil sums in a fixed order.  Results in shared memory
+// (u1 -> S.u1b and S.ub, x1 -> S.xs) and x1 -> xT.
+template <int M, bool SMC>
+__device__ __forceinline__ void kr_init_rows(const KrArgs& a, KrSmem<M>& S, float2* xl,
+                                             const float2 (&twr)[KrCfg<M>::N1], int b, int t) {
+  using Cf = KrCfg<M>;
+  constexpr int N1 = Cf::N1, N2 = Cf::N2, LPAR = Cf::LPAR, N = M;
+  const int tid = threadIdx.x, line = tid / N2, j = tid % N2, C = a.C;
+  const bool smp = S.rm[t] != 0.f;  // row t of the line mask
+  for (int c0 = 0; c0 < C; c0 += LPAR) {
+    const int c = c0 + line;
+    const bool act = c < C;
+    float2 v[N1];
+    const float2* yr = a.y + (((size_t)b * C + (act ? c : 0)) * M + t) * N;
+#pragma unroll
+    for (int s = 0; s < N1; ++s) v[s] = (act && smp) ? __ldcg(yr + specidx<M>(j, s)) : make_float2(0.f, 0.f);
+    kr_inv<M>(v, xl, twr, j);
+    if (act) {
+      float2* o = a.y1T + ((size_t)b * C + c) * N * M + t;
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) o[(size_t)(N2 * n1 + j) * M] = v[n1];
+    }
+  }
+}
+template <int M, bool SMC>
+__device__ __forceinline__ void kr_init_cols(const KrArgs& a, KrSmem<M>& S, const float2* coils, const float2* sTb,
+                                             float2* xl, const float2 (&twr)[KrCfg<M>::N1], size_t boff, int b,
+                                             int t) {
+  using Cf = KrCfg<M>;
+  constexpr int N1 = Cf::N1, N2 = Cf::N2, NT = Cf::NT, LPAR = Cf::LPAR, N = M;
+  constexpr int LW = 32 / N2, NW = NT / 32;
+  const int tid = threadIdx.x, line = tid / N2, j = tid % N2, C = a.C;
+  const float scale = rsqrtf((float)(M * N));
+  float2 acc[N1];
+  float rss[N1];
+#pragma unroll
+  for (int n1 = 0; n1 < N1; ++n1) {
+    acc[n1] = make_float2(0.f, 0.f);
+    rss[n1] = 0.f;
+  }
+  for (int c0 = 0; c0 < C; c0 += LPAR) {
+    const int c = c0 + line;
+    const bool act = c < C;
+    float2 v[N1];
+    const float2* col = a.y1T + ((size_t)b * C + (act ? c : 0)) * N * M + (size_t)t * M;
+#pragma unroll
+    for (int s = 0; s < N1; ++s) v[s] = act ? __ldcg(col + specidx<M>(j, s)) : make_float2(0.f, 0.f);
+    kr_inv<M>(v, xl, twr, j);
+    const float2* sc = SMC ? coils + (act ? c : 0) * M + j : sTb + (size_t)(act ? c : 0) * N * M + j;
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const float2 vv = cscale(v[n1], act ? scale : 0.f);
+      acc[n1] = cfmac(SMC ? sc[N2 * n1] : __ldg(sc + N2 * n1), vv, acc[n1]);  // acc += conj(s_c) v
+      rss[n1] += vv.x * vv.x + vv.y * vv.y;
+    }
+  }
+  // lines of one warp (fixed shuffle tree), then the warps in order (as kr_dataterm)
+#pragma unroll
+  for (int off = N2 * LW / 2; off >= N2; off >>= 1)
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      acc[n1].x += __shfl_xor_sync(0xffffffffu, acc[n1].x, off);
+      acc[n1].y += __shfl_xor_sync(0xffffffffu, acc[n1].y, off);
+      rss[n1] += __shfl_xor_sync(0xffffffffu, rss[n1], off);
+    }
+  __syncthreads();
+  float2* cs = S.u.xch;  // [NW][M] coil-sum partials, then [NW][M] rss partials (real parts)
+  const int wid = tid >> 5;
+  if ((tid & 31) < N2) {
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      cs[wid * M + N2 * n1 + j] = acc[n1];
+      cs[(NW + wid) * M + N2 * n1 + j] = make_float2(rss[n1], 0.f);
+    }
+  }
+  __syncthreads();
+  const int nw = (C < LPAR ? (C + LW - 1) / LW : NW);
+  for (int i = tid; i < M; i += NT) {
+    float2 u = cs[i];
+    float r = cs[NW * M + i].x;
+    for (int w = 1; w < nw; ++w) {
+      u = cadd(u, cs[w * M + i]);
+      r += cs[(NW + w) * M + i].x;
+    }
+    S.u1b[i] = u;
+    S.ub[i] = u;
+    const float2 x1 = make_float2(sqrtf(r), 0.f);
+    S.xs[i] = x1;
+    a.xT[boff + (size_t)t * M + i] = x1;
+  }
+  __syncthreads();
+}
+
 // ------------------------------------------------------------------ the kernel
 template <int M, bool SMC>
 __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_constant__ KrArgs a) {
@@ -419,7 +517,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
     unsigned long long g;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
     S.tgt0 = g;
-    S.tstage[0] = S.tstage[1] = S.tstage[2] = 0;
+    S.tstage[0] = S.tstage[1] = S.tstage[2] = S.tstage[3] = 0;
   }
   long long pclk = 0;
   auto seg = [&](int k) {  // loop segment profile (SBPCG_KR_PROF=1)
@@ -477,6 +575,13 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
   };
 
   const int n_solves = a.n_outer > 0 ? a.n_outer : 1;
+  if (a.n_outer > 0 && a.kinit) {  // Alg. 1 step 1 (u1, x1 = RSS) in this launch
+    kr_init_rows<M, SMC>(a, S, xl, twr, b, t);
+    pbar(barc, target, P);
+    kr_init_cols<M, SMC>(a, S, coils, sTb, xl, twr, boff, b, t);
+    pbar(barc, target, P);  // x1 of every column (xT) visible to the first prelude
+    stamp(3);
+  }
   for (int js = 0; js < n_solves; ++js) {
     const bool recon = a.n_outer > 0;
     const bool update_u = recon && js > 0;
@@ -494,7 +599,9 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
     const int ntj = N / TT, ntile = (M / TT) * ntj;
     const bool sbpre = recon && ntile <= P;  // one SB tile per CTA: stage its b_* now
     const int par = js & 1;
-    if (sbpre && t < ntile) {
+    if (sbpre && t < ntile && js == 0 && a.kinit) {  // fresh SB state (Alg. 1 step 1): b_* = 0
+      for (int e = tid; e < sb_pre_size<TT>(); e += NT) S.sbpre[e] = make_float2(0.f, 0.f);
+    } else if (sbpre && t < ntile) {
       SbArgs sa = a.sb;
       sa.bx_in = a.bxs[par];
       sa.by_in = a.bys[par];
@@ -505,7 +612,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
       // step writes it so), so those reads are contiguous; u and u1 of the own column stay in
       // shared memory across the solves (loaded from the image once).
       constexpr int E = (3 * M + NT - 1) / NT, EO = (M + NT - 1) / NT;
-      const bool xt = js > 0;
+      const bool xt = js > 0 || a.kinit;
       float2 xv[E], uv[EO], u1v[EO], rv[EO];
 #pragma unroll
       for (int k = 0; k < E; ++k) {
@@ -520,9 +627,9 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
         if (i < M) {
           const size_t gi = boff + (size_t)i * N + t;
           if (recon) {
-            if (js == 0) uv[k] = __ldcg(a.u + gi);
+            if (js == 0 && !a.kinit) uv[k] = __ldcg(a.u + gi);
             if (update_u) {
-              if (js == 1) u1v[k] = __ldcg(a.u1 + gi);
+              if (js == 1 && !a.kinit) u1v[k] = __ldcg(a.u1 + gi);
               rv[k] = __ldcg(a.rhs + boff + (size_t)t * M + i);
             }
           } else {
@@ -546,9 +653,9 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
         const int i = tid + k * NT;
         if (i < M) {
           if (recon) {
-            if (js == 0) S.ub[i] = uv[k];
+            if (js == 0 && !a.kinit) S.ub[i] = uv[k];
             if (update_u) {
-              if (js == 1) S.u1b[i] = u1v[k];
+              if (js == 1 && !a.kinit) S.u1b[i] = u1v[k];
               S.rhb[i] = rv[k];
             }
           } else {
@@ -1027,6 +1134,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
     a.stamp[0] += S.tstage[0];
     a.stamp[1] += S.tstage[1];
     a.stamp[2] += S.tstage[2];
+    a.stamp[5] += S.tstage[3];
     a.stamp[3] += (unsigned long long)(clock64() - S.tclk0);
     a.stamp[4] += gt1 - S.tgt0;
   }

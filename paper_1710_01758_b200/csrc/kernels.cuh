@@ -145,6 +145,9 @@ struct KrArgs {
   const float2* u1;
   float2* rhs;               // recon: rhs_reg (written by the SB phase, column-major [B][N][M])
   float2* xT;                // x, column-major [B][N][M] (internal; the image-layout x is the output)
+  int kinit;                 // recon: Alg. 1 step 1 (u1, x1 = RSS) and the zero SB state in this launch
+  const float2* y;           // kinit: zero-filled k-space [B][C][M][N]
+  float2* y1T;               // kinit: scratch [B][C][N][M] (row-inverse-transformed k-space)
   SbArgs sb;                 // recon: SB state (bx/by double buffers, bw, rhs), parity 0 first
   float2* bxs[2];
   float2* bys[2];

@@ -156,6 +156,7 @@ struct sb_ctx {
   bool kr_cg = true;            // sb_set_option(SB_OPT_PCG_CG): single-reduction recurrences in KR
   float2* sT = nullptr;         // [B][C][N][M] column-major coil maps
   unsigned* kbar = nullptr;     // [B] barrier counters
+  const float2* kr_y = nullptr;  // recon on the persistent path with kinit: the device k-space
   unsigned long long* kstamp = nullptr;  // [8] stage cycle counters
   double kr_alg_bytes = 0;      // algorithmic bytes of the timed persistent launches
   int last_path = 0;            // SB_PATH_* of the last solve / recon
@@ -1012,6 +1013,9 @@ static sb_status run_kr(sb_ctx* c, int n_outer, const sb_pcg_opts* o, int par0) 
   a.u1 = c->u1;
   a.rhs = c->rhs;
   a.xT = c->z;  // free on the persistent path
+  a.kinit = (n_outer > 0 && c->kr_y != nullptr) ? 1 : 0;
+  a.y = c->kr_y;
+  a.y1T = c->tmpc;
   a.sb.B = c->B;
   a.sb.M = c->M;
   a.sb.N = c->N;
@@ -2094,19 +2098,29 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
   }
   cudaEvent_t e0 = c->rev[0], e1 = c->rev[1];
   CK(cudaEventRecord(e0, c->st));
-  // y is always copied into the context's staging buffer so the cached graphs stay valid
-  if (!c->stage_in) CK(dalloc(&c->stage_in, c->B * c->C * c->img));
-  CK(cudaMemcpyAsync(c->stage_in, y, ybytes, is_device_ptr(y) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                     c->st));
-  const void* yd = c->stage_in;
-  // fresh SB state (Alg. 1 step 1)
-  float2* zs[] = {c->bx[0], c->bx[1], c->by[0], c->by[1], c->bw, c->rhs, c->bz[0], c->bz[1]};
-  for (auto v : zs)
-    if (v) CK(cudaMemsetAsync(v, 0, bytes, c->st));
-  CK(cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st));
-  if (c->timing) c->evnext = 0;
   const sb_pcg_opts* o = &ro->pcg;
   bool kr = use_kr(c, o);
+  // the persistent kernel does Alg. 1 step 1 and starts from a zero SB state itself (kinit)
+  const bool kinit = kr && env_flag("SBPCG_KR_INIT", true);
+  // y is copied into the context's staging buffer so the cached graphs stay valid (the
+  // persistent kernel reads a device y in place)
+  const void* yd = y;
+  if (!(kinit && is_device_ptr(y))) {
+    if (!c->stage_in) CK(dalloc(&c->stage_in, c->B * c->C * c->img));
+    CK(cudaMemcpyAsync(c->stage_in, y, ybytes, is_device_ptr(y) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       c->st));
+    yd = c->stage_in;
+  }
+  // fresh SB state (Alg. 1 step 1)
+  auto zero_state = [&]() -> sb_status {
+    float2* zs[] = {c->bx[0], c->bx[1], c->by[0], c->by[1], c->bw, c->rhs, c->bz[0], c->bz[1]};
+    for (auto v : zs)
+      if (v) CK(cudaMemsetAsync(v, 0, bytes, c->st));
+    CK(cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st));
+    return SB_OK;
+  };
+  if (!kinit && (s = zero_state())) return s;
+  if (c->timing) c->evnext = 0;
   c->stage_timing = kr ? false : (ro->stage_timers != 0);
   for (double& v : c->stage_s) v = 0.0;
   c->stage_ev.clear();
@@ -2114,16 +2128,28 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
   if (kr) {
     // Alg. 1 step 1 (u1, x = RSS) by the column/row passes, then the whole SB loop in one
     // cooperative launch (including the final shrink/Bregman step)
-    cudaEvent_t ei0 = stage_event(c), ei1 = stage_event(c);
-    CK(cudaEventRecord(ei0, c->st));
-    if ((s = seq_init_recon(c, (const float2*)yd, c->st))) return s;
-    CK(cudaEventRecord(ei1, c->st));
-    c->stage_ev.push_back({ST_INIT, {ei0, ei1}});
+    if (!kinit) {
+      cudaEvent_t ei0 = stage_event(c), ei1 = stage_event(c);
+      CK(cudaEventRecord(ei0, c->st));
+      if ((s = seq_init_recon(c, (const float2*)yd, c->st))) return s;
+      CK(cudaEventRecord(ei1, c->st));
+      c->stage_ev.push_back({ST_INIT, {ei0, ei1}});
+    }
     CK(cudaMemsetAsync(c->kstamp, 0, 32 * sizeof(unsigned long long), c->st));
+    c->kr_y = kinit ? (const float2*)yd : nullptr;
     s = run_kr(c, ro->n_outer, o, 0);
+    c->kr_y = nullptr;
     if (s == SB_E_UNSUPPORTED_SIZE && !c->kr_ok) {  // persistent launch refused: kernel sequence
       kr = false;
       c->stage_timing = ro->stage_timers != 0;
+      if (kinit) {
+        if ((s = zero_state())) return s;
+        if (yd != c->stage_in) {  // the sequence path's cached graphs read the staging buffer
+          if (!c->stage_in) CK(dalloc(&c->stage_in, c->B * c->C * c->img));
+          CK(cudaMemcpyAsync(c->stage_in, yd, ybytes, cudaMemcpyDeviceToDevice, c->st));
+          yd = c->stage_in;
+        }
+      }
     } else if (s) {
       return s;
     }
@@ -2176,6 +2202,7 @@ sb_status sb_recon(sb_ctx* c, const sb_c64* y, const sb_recon_opts* ro, sb_c64* 
     c->stage_s[ST_RHS] += s_per_cyc * (double)hst[0];
     c->stage_s[ST_PCG] += s_per_cyc * (double)hst[1];
     c->stage_s[ST_SHRINK] += s_per_cyc * (double)hst[2];
+    c->stage_s[ST_INIT] += s_per_cyc * (double)hst[5];  // Alg. 1 step 1 inside the launch (kinit)
   }
   c->stage_timing = false;
   std::vector<int32_t> li(hr.iters, hr.iters + nl);
