@@ -240,3 +240,25 @@ def test_stage_timers():
         assert sum(st.values()) <= 1.05 * log["total_ms"] * 1e-3
         assert log["build_s"] > 0
         ctx.close()
+
+
+def test_kr_in_launch_init_and_host_kspace(monkeypatch):
+    """Alg. 1 step 1 inside the persistent launch (kinit: u1, the RSS start and the zero SB state,
+    reading a device k-space in place) against the sequence-pass init followed by the launch
+    (SBPCG_KR_INIT=0): iteration counts within +-1 and images equal to the fp32 rounding of the
+    init transforms; and a host (pinned) k-space against the device one: bitwise equal."""
+    ps = batch(2, 1, (256, 256), 12, amp=100.0)
+    y = _t(np.stack([p["y"] for p in ps]))
+    res = {}
+    for mode in ("kinit", "seq", "host"):
+        monkeypatch.setenv("SBPCG_KR_INIT", "0" if mode == "seq" else "1")
+        ctx = _ctx(ps, 1.0, 0.02, 0.02, 3)
+        yy = y.cpu().pin_memory() if mode == "host" else y
+        x, log = ctx.recon(yy, 4, eps=1e-4, max_iters=50)
+        assert log["path"] == "persistent"
+        res[mode] = (_np(x), log["pcg_iters"])
+        ctx.close()
+    assert res["kinit"][1] == res["host"][1] and np.array_equal(res["kinit"][0], res["host"][0])
+    for a_, b_ in zip(res["kinit"][1], res["seq"][1]):  # init rounding differs: counts within +-1
+        assert abs(a_[0] - b_[0]) <= 1
+    assert relerr(res["kinit"][0], res["seq"][0]) <= 1e-4
