@@ -607,12 +607,28 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
       sa.by_in = a.bys[par];
       sb_tile_prefetch<TT, NT>(sa, S.sbpre, t / ntj, t % ntj, b);
     }
-    {  // one load batch: x of columns t-1, t, t+1 and u, u1, rhs_reg (or b) of column t.  After
-      // the first solve x comes from the column-major copy xT and rhs_reg is column-major (the SB
-      // step writes it so), so those reads are contiguous; u and u1 of the own column stay in
-      // shared memory across the solves (loaded from the image once).
+    const bool xt = recon && (js > 0 || a.kinit);
+    if (xt) {
+      // x of columns t-1, t, t+1 (column-major xT) and rhs_reg (column-major, written by the SB
+      // step) are copied into shared memory asynchronously; the data term runs meanwhile on the
+      // own column, already in shared memory (S.xs), and u, u1 stay in shared memory across the
+      // solves (loaded from the image once when the launch did not compute them itself)
+      for (int e = tid; e < 3 * (M / 2); e += NT) {
+        const int c = e / (M / 2), i2 = 2 * (e % (M / 2));
+        kr_cp16(&S.pc[c][i2], a.xT + boff + (size_t)((t + c - 1 + N) % N) * M + i2);
+      }
+      if (update_u)
+        for (int e = tid; e < M / 2; e += NT) kr_cp16(S.rhb + 2 * e, a.rhs + boff + (size_t)t * M + 2 * e);
+      kr_cp_commit();
+      if (!a.kinit && js == 1)
+        for (int i = tid; i < M; i += NT) S.u1b[i] = __ldcg(a.u1 + boff + (size_t)i * N + t);
+      seg(10);
+      kr_dataterm<M, SMC>(S, S.xs, coils, sTb, C, xl, twr, mbits, minv);
+      kr_cp_wait();
+      __syncthreads();
+    } else {  // the first solve without kinit, or a single solve: one synchronous load batch of
+      // x of columns t-1, t, t+1 (image layout) and u (recon) or b (solve) of column t
       constexpr int E = (3 * M + NT - 1) / NT, EO = (M + NT - 1) / NT;
-      const bool xt = js > 0 || a.kinit;
       float2 xv[E], uv[EO], u1v[EO], rv[EO];
 #pragma unroll
       for (int k = 0; k < E; ++k) {
@@ -663,10 +679,10 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
           }
         }
       }
+      __syncthreads();
+      seg(10);
+      kr_dataterm<M, SMC>(S, S.pc[1], coils, sTb, C, xl, twr, mbits, minv);
     }
-    __syncthreads();
-    seg(10);
-    kr_dataterm<M, SMC>(S, S.pc[1], coils, sTb, C, xl, twr, mbits, minv);
     seg(11);
     double d0 = 0.0, d1 = 0.0;
     for (int i = tid; i < M; i += NT) {
@@ -1084,6 +1100,7 @@ __global__ void __launch_bounds__(KrCfg<M>::NT, 2) k_persist(const __grid_consta
     if (xstore || xout)
       for (int i = tid; i < M; i += NT) {
         const float2 v = sc.zero_x ? make_float2(0.f, 0.f) : S.xs[i];
+        if (sc.zero_x) S.xs[i] = v;  // the next prelude's data term reads the own column here
         if (xstore) a.xT[boff + (size_t)t * M + i] = v;
         if (xout) a.x[boff + (size_t)i * N + t] = v;
       }
