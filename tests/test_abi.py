@@ -65,3 +65,32 @@ def test_no_oracle_on_product_path():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_binding_rejects_mismatched_arrays(lib):
+    """The binding checks dtype, shape and device of every array before an ABI call (the library
+    copies B*img or B*C*img complex values from/to the raw pointers).  A context shell with no
+    library handle exercises the check on CPU."""
+    import torch
+    from paper_1710_01758_b200.sbpcg import SbPcg
+
+    ctx = object.__new__(SbPcg)
+    ctx.B, ctx.C, ctx.image, ctx.device = 2, 3, (8, 16), torch.device("cuda", 0)
+    ok = torch.zeros((2, 8, 16), dtype=torch.complex64)
+    assert ctx._arg(ok, "x") == ok.data_ptr()                       # host tensors are allowed
+    okc = torch.zeros((2, 3, 8, 16), dtype=torch.complex64)
+    assert ctx._arg(okc, "y", coils=True) == okc.data_ptr()
+    with pytest.raises(TypeError):
+        ctx._arg(ok.to(torch.complex128), "x")                      # complex128 would overrun
+    with pytest.raises(TypeError):
+        ctx._arg(ok.numpy(), "x")                                   # not a tensor
+    with pytest.raises(ValueError):
+        ctx._arg(torch.zeros((1, 8, 16), dtype=torch.complex64), "x")  # short batch
+    with pytest.raises(ValueError):
+        ctx._arg(ok, "y", coils=True)                               # image where coils expected
+    with pytest.raises(ValueError):
+        ctx._arg(okc[:, :, :, ::2].contiguous(), "y", coils=True)   # wrong image shape
+    with pytest.raises(ValueError):
+        ctx._arg(okc.transpose(2, 3), "y", coils=True)              # non-contiguous / transposed
+    with pytest.raises(ValueError):
+        ctx._arg(torch.zeros((2, 8, 16), dtype=torch.complex64, device="meta"), "x")
