@@ -62,3 +62,25 @@ def test_binding_fails_loudly_without_the_library(tmp_path):
             "try:\n    p.SbPcg\nexcept ImportError as e:\n    print('RAISED', e)\n") % str(tmp_path)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert "RAISED" in r.stdout and "libsbpcg.so not built" in r.stdout, r.stdout + r.stderr
+
+
+def test_reference_arm_under_torchrun_world2_prints_one_line():
+    # `bench.py --impl reference` launched the way the driver launches N > 1: rank 0 alone runs
+    # the oracle and prints ONE JSON line; the other rank exits 0 without work (config 1, the
+    # small case, so the CPU suite stays short)
+    import json
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--config", "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["unit"] == "PCG iters/s"
+    assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
